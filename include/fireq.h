@@ -1,0 +1,207 @@
+/*
+ * fireq.h -- C ABI of the B200 (sm_100a) FireQ W4A8-FP linear layer.
+ *
+ * FireQ (arXiv 2505.20839).  Citations: P:NNN = line of the paper text
+ * (/root/reference/PAPER.md at build time; not needed at run time).
+ *
+ * The operation is the linear layer Y = X W^T (Eq. 3) with
+ *   - W in bf16 [N][K] (N = N_out, K = N_in) quantized OFFLINE to INT4
+ *     codes in [-8, 7] with one FP8-E4M3 scale sigma per 128 consecutive K
+ *     elements of a row (Eq. 1), after channel-wise absmean
+ *     scaling (CAS, Def. 1) and per-tensor power-of-two scaling
+ *     (PTS, Def. 2);
+ *   - X in bf16 [M][K] quantized ONLINE to FP8-E4M3 with one BF16 scale beta per
+ *     token (Eq. 2);
+ *   - the GEMM dequantizing INT4 through a 16-entry FP8 lookup table
+ *     {-8 sigma .. 7 sigma} (Step 1), multiplying on FP8 tensor cores
+ *     with FP32 accumulation (Step 2) and producing BF16 (Step 3,
+ *     P:130), with beta and the PTS inverse 2^-n applied to the output.
+ * Exact semantics (every rounding) are the readings listed in DESIGN.md.
+ *
+ * Conventions for every entry point
+ *   - All array pointers are DEVICE pointers unless marked "host".  The caller
+ *     allocates and frees every buffer; the library never allocates device
+ *     memory inside a call and never synchronizes the host.
+ *   - Work is enqueued on `stream` (a cudaStream_t passed as void*; NULL = the
+ *     legacy default stream) and is asynchronous; device faults surface at the
+ *     caller's next synchronization.
+ *   - A non-SUCCESS status means nothing was enqueued (argument errors) or a
+ *     launch failed (FIREQ_ERROR_CUDA); fireq_last_error() then returns a
+ *     thread-local human-readable detail.
+ *   - Row-major everywhere; "ld*" are leading dimensions in elements.
+ */
+#ifndef FIREQ_H_
+#define FIREQ_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    FIREQ_SUCCESS = 0,
+    FIREQ_ERROR_INVALID_VALUE = 1,      /* NULL pointer, bad enum, M < 1, ...        */
+    FIREQ_ERROR_UNSUPPORTED_SHAPE = 2,  /* N or K not a multiple of 128, too large  */
+    FIREQ_ERROR_MISALIGNED = 3,         /* pointer not 16-byte aligned / bad ld     */
+    FIREQ_ERROR_CUDA = 4,               /* a CUDA runtime/driver call failed        */
+    FIREQ_ERROR_NCCL = 5,               /* an NCCL call failed                      */
+    FIREQ_ERROR_NOT_INITIALIZED = 6,    /* comm handle missing / destroyed          */
+    FIREQ_ERROR_WORKSPACE = 7           /* workspace NULL or smaller than required  */
+} fireq_status_t;
+
+/* Status name, e.g. "FIREQ_ERROR_MISALIGNED".  Static storage. */
+const char* fireq_status_string(fireq_status_t status);
+/* Detail of the last failing call on this host thread ("" if none). */
+const char* fireq_last_error(void);
+
+/* Version of the packed weight layout produced by fireq_quantize_weight
+ * (currently 1). */
+int fireq_weight_layout_version(void);
+
+/* ------------------------------------------------------------------ sizes */
+/* Bytes of packed INT4 codes for an N x K weight: N*K/2. */
+size_t fireq_packed_weight_bytes(int64_t N, int64_t K);
+/* Bytes of FP8-E4M3 group scales: N*K/128. */
+size_t fireq_weight_scale_bytes(int64_t N, int64_t K);
+/* Device workspace needed by fireq_quantize_weight. */
+size_t fireq_quantize_weight_workspace_bytes(int64_t N, int64_t K);
+/* Device workspace needed by fireq_w4a8_gemm for this problem (split-K partial
+ * sums + per-tile arrival counters).  The counters must be ZERO before the first
+ * call that uses a workspace; every call leaves them zero again, so one
+ * cudaMemset at allocation time suffices.  A workspace must not be shared by
+ * two GEMMs that may run concurrently. */
+size_t fireq_w4a8_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
+
+/* ------------------------------------------------------- offline quantizer */
+/*
+ * fireq_quantize_weight -- steps W1..W6 (P:141-175, P:45-48,
+ * P:498-511):
+ *   W1 CAS: absmean_k = fp32(sum_n |W[n,k]| (fp64, ascending n) / N),
+ *      omega_bar = fp32(sum_k absmean_k (fp64, ascending k) / K),
+ *      lambda_k = fp32(fp64(omega_bar) / fp64(absmean_k)) (1 if absmean_k = 0);
+ *      cas_mode 0 = off (lambda = 1, the Lambda_1 case of P:152), 1 = absmean.
+ *   W2 W_bar = fp32(W) * lambda_k (one fp32 rounding).
+ *   W3 PTS: n = smallest n >= 0 with (every nonzero |W_bar| * 2^n >= 7*2^-9) or
+ *      (some 7*2^(5-n) <= |W_bar| < 7*2^(6-n)); W_tilde = W_bar * 2^n.
+ *   W4 sigma = largest E4M3 value s with 7 s <= max_group |W_tilde| (capped 448).
+ *   W5 code = clamp(round_half_even(W_tilde / sigma), -8, 7), 0 if sigma = 0.
+ *   W6 pack into layout v1.
+ * Arguments
+ *   W            bf16 [N][K], row-major, 16-B aligned.  Must be finite.
+ *   N, K         multiples of 128, N*K < 2^40.
+ *   cas_mode     0 or 1.
+ *   w_packed     out, uint8 [fireq_packed_weight_bytes(N, K)], layout v1.
+ *   w_scales     out, uint8 [fireq_weight_scale_bytes(N, K)] E4M3 codes, layout v1.
+ *   cas_lambda   out, float [K] (lambda_k), may be NULL.
+ *   cas_inv      out, bf16 [K]: c_k = bf16(1.0f / lambda_k), the Lambda^-1 that
+ *                the activation quantizer (or the previous layer) applies
+ *                (P:148-152); may be NULL.
+ *   pts_and_status  out, int32 [2]: {n, status}; status is FIREQ_SUCCESS or
+ *                FIREQ_ERROR_INVALID_VALUE (non-finite input, or no n <= 60).
+ *                The caller reads it back once (offline) and passes n to the GEMM.
+ *   workspace    >= fireq_quantize_weight_workspace_bytes(N, K) bytes.
+ */
+fireq_status_t fireq_quantize_weight(const void* W, int64_t N, int64_t K, int cas_mode,
+                                     uint8_t* w_packed, uint8_t* w_scales,
+                                     float* cas_lambda, void* cas_inv,
+                                     int32_t* pts_and_status,
+                                     void* workspace, size_t workspace_bytes,
+                                     void* stream);
+
+/* ------------------------------------------------------- online quantizer */
+/*
+ * fireq_quantize_act -- steps A1..A3 (Eq. 2; per token):
+ *   A1 x' = chan_mul ? bf16(x * c_k) : x
+ *   A2 beta_m = bf16_RN(max_k |x'| / 448), 1 if the row is all zero
+ *   A3 x_hat = E4M3_RN_satfinite(x' / beta_m)  (IEEE sign; fp32 division)
+ * Arguments
+ *   X        bf16 [M][ldx] (first K columns used), 16-B aligned, ldx % 8 == 0.
+ *   chan_mul bf16 [K] or NULL.
+ *   x_fp8    out, uint8 E4M3 [M][K] (dense, leading dimension K), 16-B aligned.
+ *   x_scale  out, bf16 [M].
+ * K % 128 == 0 (matches the GEMM), M >= 1.  Non-finite input gives
+ * unspecified output (not checked on the hot path).
+ */
+fireq_status_t fireq_quantize_act(const void* X, int64_t M, int64_t K, int64_t ldx,
+                                  const void* chan_mul, uint8_t* x_fp8, void* x_scale,
+                                  void* stream);
+
+/*
+ * fireq_silu_mul_quantize_act -- FFN helper (P:130 lists SiLU and elementwise
+ * multiplication among the epilogue operations): h = bf16(silu(g) * u) with
+ * silu(g) = g / (1 + exp(-g)) in fp32, then A2..A3 on h.  G and U are bf16
+ * [M][ld] (the gate and up projections).  Used by the FFN benchmark.
+ */
+fireq_status_t fireq_silu_mul_quantize_act(const void* G, const void* U, int64_t M, int64_t K,
+                                           int64_t ld, uint8_t* x_fp8, void* x_scale,
+                                           void* stream);
+
+/* ------------------------------------------------------------------ GEMM */
+/*
+ * fireq_w4a8_gemm -- Steps 1..3 of the INT4 x FP8 kernel:
+ *   y[m][n] = bf16_RN( acc[m][n] * (beta_m * 2^-pts_exponent) [* gamma_n] )
+ *   acc[m][n] = sum_k dec(x_fp8[m][k]) * dec(LUT_{n, k/128}[code[n][k]]) in FP32
+ *   LUT_{n,g}[v] = E4M3_RN(v * sigma_{n,g}), v in [-8, 7].
+ * The FP32 accumulation order is the tensor core's (tolerance-checked, G4).
+ * Arguments
+ *   x_fp8        uint8 E4M3 [M][K] dense (from fireq_quantize_act), 16-B aligned.
+ *   x_scale      bf16 [M] (beta).
+ *   M            >= 1 tokens.   K: multiple of 128, <= 65536.
+ *   w_packed, w_scales  from fireq_quantize_weight (layout v1), N multiple of 128.
+ *   pts_exponent host int n in [0, 60] (pts_and_status[0]).
+ *   out_chan_scale  float [N] gamma or NULL.
+ *   Y            out bf16: out_layout 0 -> Y[M][ldy] (ldy >= N), 1 -> Y^T [N][ldy]
+ *                (ldy >= M).  ldy % 8 == 0, 16-B aligned.  Rows/cols outside
+ *                [0,M) x [0,N) are never written.
+ *   workspace    >= fireq_w4a8_gemm_workspace_bytes(M, N, K) (see there).
+ */
+fireq_status_t fireq_w4a8_gemm(const uint8_t* x_fp8, const void* x_scale, int64_t M, int64_t K,
+                               const uint8_t* w_packed, const uint8_t* w_scales, int64_t N,
+                               int32_t pts_exponent, const float* out_chan_scale,
+                               void* Y, int64_t ldy, int out_layout,
+                               void* workspace, size_t workspace_bytes, void* stream);
+
+/* --------------------------------------------------------- multi-GPU layer */
+/* Opaque NCCL communicator wrapper (caller-owned, not thread-safe). */
+typedef struct fireq_comm* fireq_comm_t;
+
+/* host: writes a 128-byte NCCL unique id into id[128] (rank 0 calls it and
+ * broadcasts the bytes by any host means). */
+fireq_status_t fireq_comm_get_unique_id(uint8_t id[128]);
+/* host: collective over nranks processes, one GPU each (the current device). */
+fireq_status_t fireq_comm_init(fireq_comm_t* out, int nranks, int rank, const uint8_t id[128]);
+fireq_status_t fireq_comm_destroy(fireq_comm_t comm);
+
+/*
+ * fireq_w4a8_gemm_colpar -- column-parallel (N-sharded) linear layer
+ * (BASELINE north_star (d)): this rank holds rows [rank*N_local, (rank+1)*N_local)
+ * of the quantized weight (byte slices of the full packing, layout v1, because
+ * CAS lambda and PTS n are computed on the full tensor before sharding).  X is
+ * replicated.  The rank computes its slice with fireq_w4a8_gemm in the Y^T
+ * layout directly into its slot of Yt_full [N_local*nranks][M] and an in-place
+ * ncclAllGather (bf16) over NVLink completes Y^T on every rank, on `stream`.
+ *   Yt_full   out bf16 [nranks*N_local][M] (Y^T, ld = M).
+ */
+fireq_status_t fireq_w4a8_gemm_colpar(const uint8_t* x_fp8, const void* x_scale, int64_t M,
+                                      int64_t K, const uint8_t* w_packed_local,
+                                      const uint8_t* w_scales_local, int64_t N_local,
+                                      int32_t pts_exponent, void* Yt_full,
+                                      void* workspace, size_t workspace_bytes,
+                                      fireq_comm_t comm, void* stream);
+
+/* --------------------------------------------------------- introspection */
+/* Debug/test: writes the 127 x 16 LUT-of-LUTs the GEMM builds on chip
+ * (entry [s][u] = E4M3_RN(v(u) * dec(s)), v(u) = u < 8 ? u : u - 16) into the
+ * device buffer out[2032], on `stream`. */
+fireq_status_t fireq_debug_lut_table(uint8_t* out, void* stream);
+/* Number of GEMM kernel launches fireq_w4a8_gemm would enqueue for (M, N, K)
+ * and the chosen configuration, for benchmarks: writes {ntok, splits, ctas,
+ * sign_split} into cfg_out[4] (host). */
+fireq_status_t fireq_gemm_plan(int64_t M, int64_t N, int64_t K, int32_t cfg_out[4]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FIREQ_H_ */

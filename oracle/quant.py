@@ -163,8 +163,10 @@ class QuantizedWeight:
         self.__dict__.update(kw)
 
 
-def quantize_weight(W, cas_mode):
+def quantize_weight(W, cas_mode, pack=True):
     """W1-W6 for a bf16 weight matrix W [N][K] (float64 array of bf16 values).
+
+    pack=False skips W6 (packed/scales are None) for large sampled checks.
 
     Returns QuantizedWeight with: lam (fp32 values), c (bf16 values),
     n (PTS exponent), reason, sigma [N][G] (values), sigma_codes [N][G],
@@ -184,8 +186,8 @@ def quantize_weight(W, cas_mode):
     sigma_codes = e4m3_encode(sigma)
     return QuantizedWeight(lam=lam, c=c, n=n, reason=reason, W_bar=W_bar,
                            sigma=sigma, sigma_codes=sigma_codes, codes=codes,
-                           packed=layout.pack_codes(codes),
-                           scales=layout.pack_scales(sigma_codes))
+                           packed=layout.pack_codes(codes) if pack else None,
+                           scales=layout.pack_scales(sigma_codes) if pack else None)
 
 
 # ------------------------------------------------------------------- A1 .. A3

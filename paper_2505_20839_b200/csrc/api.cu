@@ -1,0 +1,280 @@
+// api.cu -- the extern "C" boundary of libfireq.so (include/fireq.h): argument
+// validation, status codes, thread-local error detail, sizes, and the NCCL-based
+// column-parallel layer.  NCCL is resolved at run time with dlopen("libnccl.so.2")
+// so the library shares the NCCL already loaded by the host process (torch).
+#include <dlfcn.h>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+
+namespace fireq {
+
+// implemented in the kernel translation units
+fireq_status_t quantize_weight_impl(const __nv_bfloat16* W, int64_t N, int64_t K, int cas_mode, uint8_t* w_packed,
+                                    uint8_t* w_scales, float* cas_lambda, __nv_bfloat16* cas_inv,
+                                    int32_t* pts_and_status, void* ws, cudaStream_t stream);
+size_t wq_workspace_bytes(int64_t K);
+fireq_status_t quantize_act_impl(const __nv_bfloat16* X, const __nv_bfloat16* U, int64_t M, int64_t K, int64_t ld,
+                                 const __nv_bfloat16* c, int mode, uint8_t* xq, __nv_bfloat16* beta,
+                                 cudaStream_t stream);
+size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
+fireq_status_t gemm_plan(int64_t M, int64_t N, int64_t K, int32_t* cfg);
+fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int64_t M, int64_t K,
+                         const uint8_t* w_packed, const uint8_t* w_scales, int64_t N, int32_t pts_n,
+                         const float* gamma, __nv_bfloat16* Y, int64_t ldy, int out_layout, void* ws,
+                         size_t ws_bytes, cudaStream_t stream);
+fireq_status_t debug_lut_table(uint8_t* out, cudaStream_t stream);
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error_c() { return g_last_error.c_str(); }
+
+fireq_status_t fail(fireq_status_t st, const std::string& msg) {
+    g_last_error = msg;
+    return st;
+}
+
+fireq_status_t check_launch(const char* what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(FIREQ_ERROR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return FIREQ_SUCCESS;
+}
+
+int sm_count() {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+}
+
+int max_smem_optin() {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return n;
+}
+
+}  // namespace fireq
+
+using namespace fireq;
+
+#define FIREQ_REQUIRE(cond, status, msg) \
+    do {                                 \
+        if (!(cond)) return fail((status), (msg)); \
+    } while (0)
+
+extern "C" {
+
+const char* fireq_status_string(fireq_status_t s) {
+    switch (s) {
+        case FIREQ_SUCCESS: return "FIREQ_SUCCESS";
+        case FIREQ_ERROR_INVALID_VALUE: return "FIREQ_ERROR_INVALID_VALUE";
+        case FIREQ_ERROR_UNSUPPORTED_SHAPE: return "FIREQ_ERROR_UNSUPPORTED_SHAPE";
+        case FIREQ_ERROR_MISALIGNED: return "FIREQ_ERROR_MISALIGNED";
+        case FIREQ_ERROR_CUDA: return "FIREQ_ERROR_CUDA";
+        case FIREQ_ERROR_NCCL: return "FIREQ_ERROR_NCCL";
+        case FIREQ_ERROR_NOT_INITIALIZED: return "FIREQ_ERROR_NOT_INITIALIZED";
+        case FIREQ_ERROR_WORKSPACE: return "FIREQ_ERROR_WORKSPACE";
+    }
+    return "FIREQ_ERROR_UNKNOWN";
+}
+
+const char* fireq_last_error(void) { return fireq::last_error_c(); }
+
+int fireq_weight_layout_version(void) { return 1; }
+
+size_t fireq_packed_weight_bytes(int64_t N, int64_t K) { return (N > 0 && K > 0) ? (size_t)(N * K / 2) : 0; }
+size_t fireq_weight_scale_bytes(int64_t N, int64_t K) { return (N > 0 && K > 0) ? (size_t)(N * K / 128) : 0; }
+size_t fireq_quantize_weight_workspace_bytes(int64_t N, int64_t K) {
+    (void)N;
+    return K > 0 ? wq_workspace_bytes(K) : 0;
+}
+size_t fireq_w4a8_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
+    if (M < 1 || N < 128 || K < 128) return 0;
+    return gemm_workspace_bytes(M, N, K);
+}
+
+fireq_status_t fireq_quantize_weight(const void* W, int64_t N, int64_t K, int cas_mode, uint8_t* w_packed,
+                                     uint8_t* w_scales, float* cas_lambda, void* cas_inv, int32_t* pts_and_status,
+                                     void* workspace, size_t workspace_bytes, void* stream) {
+    FIREQ_REQUIRE(W && w_packed && w_scales && pts_and_status, FIREQ_ERROR_INVALID_VALUE,
+                  "fireq_quantize_weight: NULL required pointer");
+    FIREQ_REQUIRE(cas_mode == 0 || cas_mode == 1, FIREQ_ERROR_INVALID_VALUE, "fireq_quantize_weight: cas_mode must be 0 or 1");
+    FIREQ_REQUIRE(N >= 128 && K >= 128 && N % 128 == 0 && K % 128 == 0, FIREQ_ERROR_UNSUPPORTED_SHAPE,
+                  "fireq_quantize_weight: N and K must be positive multiples of 128");
+    FIREQ_REQUIRE(N * K < (int64_t(1) << 40), FIREQ_ERROR_UNSUPPORTED_SHAPE, "fireq_quantize_weight: N*K too large");
+    FIREQ_REQUIRE(aligned16(W) && aligned16(w_packed), FIREQ_ERROR_MISALIGNED,
+                  "fireq_quantize_weight: W and w_packed must be 16-byte aligned");
+    FIREQ_REQUIRE(workspace && workspace_bytes >= wq_workspace_bytes(K), FIREQ_ERROR_WORKSPACE,
+                  "fireq_quantize_weight: workspace too small");
+    return quantize_weight_impl(static_cast<const __nv_bfloat16*>(W), N, K, cas_mode, w_packed, w_scales, cas_lambda,
+                                static_cast<__nv_bfloat16*>(cas_inv), pts_and_status, workspace,
+                                static_cast<cudaStream_t>(stream));
+}
+
+static fireq_status_t check_act_args(const void* X, int64_t M, int64_t K, int64_t ldx, uint8_t* x_fp8,
+                                     void* x_scale, const char* who) {
+    FIREQ_REQUIRE(X && x_fp8 && x_scale, FIREQ_ERROR_INVALID_VALUE, std::string(who) + ": NULL required pointer");
+    FIREQ_REQUIRE(M >= 1, FIREQ_ERROR_INVALID_VALUE, std::string(who) + ": M must be >= 1");
+    FIREQ_REQUIRE(K >= 128 && K % 128 == 0 && K <= 65536, FIREQ_ERROR_UNSUPPORTED_SHAPE,
+                  std::string(who) + ": K must be a multiple of 128 in [128, 65536]");
+    FIREQ_REQUIRE(ldx >= K && ldx % 8 == 0 && aligned16(X) && aligned16(x_fp8), FIREQ_ERROR_MISALIGNED,
+                  std::string(who) + ": X/x_fp8 must be 16-byte aligned, ldx >= K and ldx % 8 == 0");
+    return FIREQ_SUCCESS;
+}
+
+fireq_status_t fireq_quantize_act(const void* X, int64_t M, int64_t K, int64_t ldx, const void* chan_mul,
+                                  uint8_t* x_fp8, void* x_scale, void* stream) {
+    fireq_status_t st = check_act_args(X, M, K, ldx, x_fp8, x_scale, "fireq_quantize_act");
+    if (st != FIREQ_SUCCESS) return st;
+    FIREQ_REQUIRE(!chan_mul || aligned16(chan_mul), FIREQ_ERROR_MISALIGNED, "fireq_quantize_act: chan_mul must be 16-byte aligned");
+    return quantize_act_impl(static_cast<const __nv_bfloat16*>(X), nullptr, M, K, ldx,
+                             static_cast<const __nv_bfloat16*>(chan_mul), chan_mul ? 1 : 0, x_fp8,
+                             static_cast<__nv_bfloat16*>(x_scale), static_cast<cudaStream_t>(stream));
+}
+
+fireq_status_t fireq_silu_mul_quantize_act(const void* G, const void* U, int64_t M, int64_t K, int64_t ld,
+                                           uint8_t* x_fp8, void* x_scale, void* stream) {
+    fireq_status_t st = check_act_args(G, M, K, ld, x_fp8, x_scale, "fireq_silu_mul_quantize_act");
+    if (st != FIREQ_SUCCESS) return st;
+    FIREQ_REQUIRE(U && aligned16(U), FIREQ_ERROR_MISALIGNED, "fireq_silu_mul_quantize_act: U must be 16-byte aligned");
+    return quantize_act_impl(static_cast<const __nv_bfloat16*>(G), static_cast<const __nv_bfloat16*>(U), M, K, ld,
+                             nullptr, 2, x_fp8, static_cast<__nv_bfloat16*>(x_scale),
+                             static_cast<cudaStream_t>(stream));
+}
+
+fireq_status_t fireq_w4a8_gemm(const uint8_t* x_fp8, const void* x_scale, int64_t M, int64_t K,
+                               const uint8_t* w_packed, const uint8_t* w_scales, int64_t N, int32_t pts_exponent,
+                               const float* out_chan_scale, void* Y, int64_t ldy, int out_layout, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+    FIREQ_REQUIRE(x_fp8 && x_scale && w_packed && w_scales && Y && workspace, FIREQ_ERROR_INVALID_VALUE,
+                  "fireq_w4a8_gemm: NULL required pointer");
+    FIREQ_REQUIRE(M >= 1 && M <= (int64_t(1) << 24), FIREQ_ERROR_INVALID_VALUE, "fireq_w4a8_gemm: M must be in [1, 2^24]");
+    FIREQ_REQUIRE(out_layout == 0 || out_layout == 1, FIREQ_ERROR_INVALID_VALUE, "fireq_w4a8_gemm: out_layout must be 0 or 1");
+    FIREQ_REQUIRE(pts_exponent >= 0 && pts_exponent <= 60, FIREQ_ERROR_INVALID_VALUE,
+                  "fireq_w4a8_gemm: pts_exponent must be in [0, 60]");
+    FIREQ_REQUIRE(K >= 128 && K % 128 == 0 && K <= 65536 && N >= 128 && N % 128 == 0 && N <= (int64_t(1) << 20),
+                  FIREQ_ERROR_UNSUPPORTED_SHAPE, "fireq_w4a8_gemm: N, K must be multiples of 128 (K <= 65536)");
+    FIREQ_REQUIRE(aligned16(x_fp8) && aligned16(w_packed) && aligned16(w_scales) && aligned16(Y) && ldy % 8 == 0 &&
+                      (out_layout == 0 ? ldy >= N : ldy >= M),
+                  FIREQ_ERROR_MISALIGNED, "fireq_w4a8_gemm: pointers must be 16-byte aligned, ldy % 8 == 0 and large enough");
+    return gemm_impl(x_fp8, static_cast<const __nv_bfloat16*>(x_scale), M, K, w_packed, w_scales, N, pts_exponent,
+                     out_chan_scale, static_cast<__nv_bfloat16*>(Y), ldy, out_layout, workspace, workspace_bytes,
+                     static_cast<cudaStream_t>(stream));
+}
+
+fireq_status_t fireq_debug_lut_table(uint8_t* out, void* stream) {
+    FIREQ_REQUIRE(out, FIREQ_ERROR_INVALID_VALUE, "fireq_debug_lut_table: NULL pointer");
+    return debug_lut_table(out, static_cast<cudaStream_t>(stream));
+}
+
+fireq_status_t fireq_gemm_plan(int64_t M, int64_t N, int64_t K, int32_t cfg_out[4]) {
+    FIREQ_REQUIRE(cfg_out && M >= 1 && N % 128 == 0 && K % 128 == 0 && N > 0 && K > 0, FIREQ_ERROR_INVALID_VALUE,
+                  "fireq_gemm_plan: bad arguments");
+    return gemm_plan(M, N, K, cfg_out);
+}
+
+// ------------------------------------------------------------------ NCCL layer
+typedef struct { char internal[128]; } nccl_uid_t;
+typedef void* nccl_comm_raw_t;
+typedef int (*pfn_get_uid)(nccl_uid_t*);
+typedef int (*pfn_init_rank)(nccl_comm_raw_t*, int, nccl_uid_t, int);
+typedef int (*pfn_destroy)(nccl_comm_raw_t);
+typedef int (*pfn_allgather)(const void*, void*, size_t, int, nccl_comm_raw_t, cudaStream_t);
+typedef const char* (*pfn_errstr)(int);
+
+struct NcclApi {
+    bool ok = false;
+    pfn_get_uid get_uid = nullptr;
+    pfn_init_rank init_rank = nullptr;
+    pfn_destroy destroy = nullptr;
+    pfn_allgather allgather = nullptr;
+    pfn_errstr errstr = nullptr;
+};
+
+static NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        api.get_uid = (pfn_get_uid)dlsym(h, "ncclGetUniqueId");
+        api.init_rank = (pfn_init_rank)dlsym(h, "ncclCommInitRank");
+        api.destroy = (pfn_destroy)dlsym(h, "ncclCommDestroy");
+        api.allgather = (pfn_allgather)dlsym(h, "ncclAllGather");
+        api.errstr = (pfn_errstr)dlsym(h, "ncclGetErrorString");
+        api.ok = api.get_uid && api.init_rank && api.destroy && api.allgather;
+    });
+    return api;
+}
+
+struct fireq_comm {
+    nccl_comm_raw_t comm = nullptr;
+    int nranks = 0;
+    int rank = 0;
+};
+
+static fireq_status_t nccl_fail(int r, const char* what) {
+    const char* s = nccl().errstr ? nccl().errstr(r) : "?";
+    return fail(FIREQ_ERROR_NCCL, std::string(what) + ": " + s);
+}
+
+fireq_status_t fireq_comm_get_unique_id(uint8_t id[128]) {
+    FIREQ_REQUIRE(id, FIREQ_ERROR_INVALID_VALUE, "fireq_comm_get_unique_id: NULL id");
+    FIREQ_REQUIRE(nccl().ok, FIREQ_ERROR_NCCL, "libnccl.so.2 not found");
+    nccl_uid_t uid;
+    const int r = nccl().get_uid(&uid);
+    if (r != 0) return nccl_fail(r, "ncclGetUniqueId");
+    memcpy(id, uid.internal, 128);
+    return FIREQ_SUCCESS;
+}
+
+fireq_status_t fireq_comm_init(fireq_comm_t* out, int nranks, int rank, const uint8_t id[128]) {
+    FIREQ_REQUIRE(out && id && nranks >= 1 && rank >= 0 && rank < nranks, FIREQ_ERROR_INVALID_VALUE,
+                  "fireq_comm_init: bad arguments");
+    FIREQ_REQUIRE(nccl().ok, FIREQ_ERROR_NCCL, "libnccl.so.2 not found");
+    nccl_uid_t uid;
+    memcpy(uid.internal, id, 128);
+    fireq_comm* c = new fireq_comm();
+    const int r = nccl().init_rank(&c->comm, nranks, uid, rank);
+    if (r != 0) {
+        delete c;
+        return nccl_fail(r, "ncclCommInitRank");
+    }
+    c->nranks = nranks;
+    c->rank = rank;
+    *out = c;
+    return FIREQ_SUCCESS;
+}
+
+fireq_status_t fireq_comm_destroy(fireq_comm_t comm) {
+    FIREQ_REQUIRE(comm, FIREQ_ERROR_NOT_INITIALIZED, "fireq_comm_destroy: NULL comm");
+    const int r = nccl().destroy(comm->comm);
+    delete comm;
+    if (r != 0) return nccl_fail(r, "ncclCommDestroy");
+    return FIREQ_SUCCESS;
+}
+
+fireq_status_t fireq_w4a8_gemm_colpar(const uint8_t* x_fp8, const void* x_scale, int64_t M, int64_t K,
+                                      const uint8_t* w_packed_local, const uint8_t* w_scales_local, int64_t N_local,
+                                      int32_t pts_exponent, void* Yt_full, void* workspace, size_t workspace_bytes,
+                                      fireq_comm_t comm, void* stream) {
+    FIREQ_REQUIRE(comm && comm->comm, FIREQ_ERROR_NOT_INITIALIZED, "fireq_w4a8_gemm_colpar: comm not initialized");
+    FIREQ_REQUIRE(M % 8 == 0, FIREQ_ERROR_MISALIGNED, "fireq_w4a8_gemm_colpar: M must be a multiple of 8 (Y^T rows)");
+    // Y^T: rank r's slice [r*N_local, (r+1)*N_local) x M is contiguous: write it in place.
+    __nv_bfloat16* slot = static_cast<__nv_bfloat16*>(Yt_full) + (size_t)comm->rank * N_local * M;
+    fireq_status_t st = fireq_w4a8_gemm(x_fp8, x_scale, M, K, w_packed_local, w_scales_local, N_local, pts_exponent,
+                                        nullptr, slot, M, 1, workspace, workspace_bytes, stream);
+    if (st != FIREQ_SUCCESS) return st;
+    if (comm->nranks == 1) return FIREQ_SUCCESS;
+    const int r = nccl().allgather(slot, Yt_full, (size_t)N_local * M, /*ncclBfloat16=*/9, comm->comm,
+                                   static_cast<cudaStream_t>(stream));
+    if (r != 0) return nccl_fail(r, "ncclAllGather");
+    return FIREQ_SUCCESS;
+}
+
+}  // extern "C"

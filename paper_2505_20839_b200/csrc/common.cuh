@@ -1,0 +1,45 @@
+// common.cuh -- shared device helpers and host-side status plumbing for libfireq.
+#pragma once
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include "../../include/fireq.h"
+
+namespace fireq {
+
+// --------------------------------------------------------------- host status
+void set_error(const std::string& msg);
+fireq_status_t fail(fireq_status_t st, const std::string& msg);
+fireq_status_t check_launch(const char* what);
+int sm_count();
+int max_smem_optin();
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// --------------------------------------------------------------- device math
+// E4M3 code -> float, from the bit fields (exact).
+__device__ __forceinline__ float e4m3_decode(uint32_t c) {
+    const uint32_t e = (c >> 3) & 0xF, f = c & 7;
+    const float mag = e ? __int_as_float(((e + 120u) << 23) | (f << 20))  // (1+f/8)*2^(e-7)
+                        : (float)f * 0x1p-9f;                              // subnormal f*2^-9
+    return (c & 0x80) ? -mag : mag;
+}
+// float -> E4M3 code, round to nearest even, saturate to +-448 (hardware cvt).
+__device__ __forceinline__ uint32_t e4m3_rn(float x) {
+    uint16_t r;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(0.0f), "f"(x));
+    return r & 0xFFu;
+}
+// two floats -> two E4M3 codes packed as (hi << 8) | lo
+__device__ __forceinline__ uint32_t e4m3x2_rn(float lo, float hi) {
+    uint16_t r;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+// 2^-n for 0 <= n <= 126, exact.
+__device__ __forceinline__ float exp2_neg(int n) { return __int_as_float((127 - n) << 23); }
+
+}  // namespace fireq

@@ -1,0 +1,568 @@
+// gemm.cu -- fireq_w4a8_gemm: the INT4 x FP8 linear layer on sm_100a tensor cores.
+//
+// The paper's three steps mapped onto Blackwell:
+//   Step 1  TMA stages packed INT4 weights (layout v1: one 8 KiB bulk copy per
+//           128-row x 128-K block), their FP8 scales and FP8 activation tiles into a
+//           shared-memory ring; CUDA-core converter warps turn INT4 codes into
+//           FP8 bytes through the per-group 16-entry LUT with byte permutes (prmt)
+//           and store them straight into TENSOR MEMORY (tcgen05.st) as the MMA's
+//           A operand (thread t of a converter warpgroup <-> weight row t <-> TMEM
+//           lane t).
+//   Step 2  One thread issues tcgen05.mma.kind::f8f6f4 (E4M3 x E4M3, FP32
+//           accumulation in TMEM): D[128 weight rows][NTOK tokens] += A[tmem] * B[smem].
+//           "Swap-AB": weights are the MMA M side, tokens the N side, so decode
+//           batches (M = 16) use N_mma = 16 without waste on the weight side.
+//   Step 3  Epilogue warps tcgen05.ld the accumulator, apply beta_m * 2^-n (* gamma_n)
+//           in FP32, round once to BF16 and store Y (or Y^T).
+//
+// Converter schemes:
+//   sign-split (decode, NTOK <= 128): P = prmt(LUT[0..7], w) gives the entries of
+//     non-negative codes (0x00 for negative ones, because POS bytes have msb 0 and
+//     prmt's selector bit 3 replicates the msb), NEGMAG = prmt(|LUT[8..15]|, w^0x88888888)
+//     the magnitudes of negative codes; D += P*B and D += (-NEGMAG)*B (idesc negate-A).
+//     4 PRMT + 1 LOP3 (ALU pipe) + 2 IMAD.HI (FMA pipe) per 8 codes.
+//   mask-select (prefill): one operand; R = mux(prmt(POS,w), prmt(NEG,w^0x88..), mask)
+//     with the per-byte sign mask made by prmt's sign-replicate mode from w and w<<4.
+//
+// Work distribution: persistent, one CTA per SM.  Work units are (tile, 128-K group);
+// tiles are round-robin over CTAs when there are many, otherwise units are split
+// contiguously across CTAs ("stream-K"), and tiles shared by several CTAs are
+// reduced deterministically (fixed contributor order) by the last-arriving CTA.
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace fireq {
+namespace {
+
+constexpr int kGroup = 128;            // K per group (one FP8 scale)
+constexpr int kTileN = 128;            // weight rows per tile = MMA M
+constexpr int kWBytes = kTileN * kGroup / 2;   // 8192 packed bytes per (tile, group)
+constexpr int kLutEntries = 127 * 16;
+
+struct GemmArgs {
+    const uint8_t* w_packed;
+    const uint8_t* w_scales;
+    const __nv_bfloat16* x_scale;
+    const float* gamma;
+    __nv_bfloat16* Y;
+    float* partial;        // [2*C][NTOK][128] fp32 (stream-K only)
+    unsigned* counters;    // [tiles]
+    int64_t ldy;
+    int M, N, K, G;
+    int n_tiles, m_tiles, tiles;
+    int pts_n;
+    int out_layout;
+    int mode;              // 0 = tile round-robin, 1 = stream-K
+    int C;                 // CTAs in the grid
+    long long U;           // total units (stream-K)
+};
+
+// Segment = contiguous run of groups [g0, g1) of one tile processed by one CTA.
+struct SegIter {
+    int mode, G, tiles, C, c, k;
+    long long u, u_end;
+    __device__ __forceinline__ void init(const GemmArgs& a, int cta) {
+        mode = a.mode; G = a.G; tiles = a.tiles; C = a.C; c = cta; k = 0;
+        u = (long long)cta * a.U / a.C;
+        u_end = (long long)(cta + 1) * a.U / a.C;
+    }
+    __device__ __forceinline__ bool next(int& tile, int& g0, int& g1) {
+        if (mode == 0) {
+            tile = c + k * C;
+            if (tile >= tiles) return false;
+            ++k; g0 = 0; g1 = G;
+            return true;
+        }
+        if (u >= u_end) return false;
+        tile = (int)(u / G);
+        g0 = (int)(u % G);
+        g1 = (int)min((long long)G, (long long)g0 + (u_end - u));
+        u = (long long)tile * G + g1;
+        return true;
+    }
+};
+
+// CTA owning unit u under the contiguous split.
+__device__ __forceinline__ int owner_of(long long u, long long U, int C) {
+    int c = (int)((u * C) / U);
+    while (c + 1 < C && (long long)(c + 1) * U / C <= u) ++c;
+    while (c > 0 && (long long)c * U / C > u) --c;
+    return c;
+}
+
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row core groups 1024 B apart.
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;                  // LBO (unused for swizzled K-major) = 16 B
+    d |= (uint64_t)(1024 >> 4) << 32;        // SBO = 1024 B
+    d |= (uint64_t)1 << 46;                  // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;                  // SWIZZLE_128B
+    return d;
+}
+
+// Instruction descriptor, kind::f8f6f4: E4M3 x E4M3 -> F32, K-major A and B, M = 128.
+__host__ __device__ constexpr uint32_t make_idesc(int ntok, bool negate_a) {
+    return (1u << 4)                          // D format F32
+         | (0u << 7) | (0u << 10)             // A, B = E4M3
+         | ((negate_a ? 1u : 0u) << 13)
+         | ((uint32_t)(ntok >> 3) << 17)      // N >> 3
+         | ((uint32_t)(128 >> 4) << 24);      // M >> 4
+}
+
+template <int NTOK, bool SIGN_SPLIT, int NCONV, int STAGES, int ASTAGES, int ACCBUF>
+struct Cfg {
+    static constexpr int kXBytes = NTOK * kGroup;                       // FP8 activation tile
+    static constexpr int kStageTx = kXBytes + kWBytes + kTileN;         // bytes per stage
+    static constexpr int kASz = SIGN_SPLIT ? 64 : 32;                   // TMEM cols per A stage
+    static constexpr int kAccCols = ACCBUF * NTOK;
+    static constexpr int kACol0 = (kAccCols + 31) / 32 * 32;
+    static constexpr int kTmemNeed = kACol0 + ASTAGES * kASz;
+    static constexpr int kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128
+                                   : kTmemNeed <= 256 ? 256 : 512;
+    static_assert(kTmemNeed <= 512, "TMEM budget");
+    static constexpr int kThreads = 256 + 128 * NCONV;
+    // shared memory carve-up (offsets from a 1024-aligned base)
+    static constexpr int kOffX = 0;
+    static constexpr int kOffW = kOffX + STAGES * kXBytes;
+    static constexpr int kOffS = kOffW + STAGES * kWBytes;
+    static constexpr int kOffLut = kOffS + STAGES * kTileN;
+    static constexpr int kOffBar = kOffLut + 2048;
+    static constexpr int kNumBars = 2 * STAGES + 2 * ASTAGES + 2 * ACCBUF;
+    static constexpr int kOffMisc = kOffBar + kNumBars * 8;
+    static constexpr int kSmemBytes = kOffMisc + 64 + 1024;             // + alignment slack
+    static_assert(kXBytes % 1024 == 0, "X tile must keep 1024-B alignment");
+};
+
+// 16 output bytes pair (lo/hi word) per input word, sign-split.
+__device__ __forceinline__ void conv_sign_split(uint32_t w, uint32_t L0, uint32_t L1, uint32_t N0, uint32_t N1,
+                                                uint32_t& p0, uint32_t& p1, uint32_t& n0, uint32_t& n1) {
+    const uint32_t x = w ^ 0x88888888u;
+    const uint32_t wh = ptx::hi16_fma(w);
+    const uint32_t xh = ptx::hi16_fma(x);
+    p0 = ptx::prmt(L0, L1, w);
+    p1 = ptx::prmt(L0, L1, wh);
+    n0 = ptx::prmt(N0, N1, x);
+    n1 = ptx::prmt(N0, N1, xh);
+}
+
+__device__ __forceinline__ void conv_mask_select(uint32_t w, uint32_t L0, uint32_t L1, uint32_t L2, uint32_t L3,
+                                                 uint32_t& r0, uint32_t& r1) {
+    const uint32_t x = w ^ 0x88888888u;
+    const uint32_t t = ptx::shl4_fma(w);
+    const uint32_t wh = ptx::hi16_fma(w);
+    const uint32_t xh = ptx::hi16_fma(x);
+    const uint32_t m0 = ptx::prmt(w, t, 0x9D8Cu);     // 0xFF where nibble 0..3 is negative
+    const uint32_t m1 = ptx::prmt(w, t, 0xBFAEu);     // nibbles 4..7
+    r0 = ptx::lop3_mux(ptx::prmt(L0, L1, w), ptx::prmt(L2, L3, x), m0);
+    r1 = ptx::lop3_mux(ptx::prmt(L0, L1, wh), ptx::prmt(L2, L3, xh), m1);
+}
+
+template <int NTOK, bool SIGN_SPLIT, int NCONV, int STAGES, int ASTAGES, int ACCBUF>
+__global__ void __launch_bounds__(Cfg<NTOK, SIGN_SPLIT, NCONV, STAGES, ASTAGES, ACCBUF>::kThreads, 1)
+k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
+    using C = Cfg<NTOK, SIGN_SPLIT, NCONV, STAGES, ASTAGES, ACCBUF>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-B alignment for the SW128 tiles, computed on the shared-window address so
+    // that the pointer stays visibly in the shared state space (LDS, not generic LD).
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* sX = smem + C::kOffX;
+    uint8_t* sW = smem + C::kOffW;
+    uint8_t* sS = smem + C::kOffS;
+    uint4* sLut = reinterpret_cast<uint4*>(smem + C::kOffLut);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+    uint64_t* full = bars;
+    uint64_t* empty = full + STAGES;
+    uint64_t* afull = empty + STAGES;
+    uint64_t* aempty = afull + ASTAGES;
+    uint64_t* accfull = aempty + ASTAGES;
+    uint64_t* accempty = accfull + ACCBUF;
+    uint32_t* misc = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);   // [0] tmem base, [1] fixup flag
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    // ------------------------------------------------------------ setup
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < STAGES; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], 1); }
+        for (int i = 0; i < ASTAGES; ++i) { ptx::mbar_init(&afull[i], 128); ptx::mbar_init(&aempty[i], 1); }
+        for (int i = 0; i < ACCBUF; ++i) { ptx::mbar_init(&accfull[i], 1); ptx::mbar_init(&accempty[i], 128); }
+        ptx::fence_mbar_init();
+        ptx::prefetch_tmap(&tmap_x);
+    }
+    if (warp == 2) {
+        ptx::tmem_alloc(&misc[0], C::kTmemCols);
+        ptx::tmem_relinquish();
+    }
+    if (warp == 2 || warp == 3) {
+        // LUT-of-LUTs: entry [s][u] = E4M3_RN(v(u) * sigma_s) for all 127 finite sigma codes
+        // (Step 1's 16-entry table).  v * sigma is exact in fp32.
+        uint8_t* lut = reinterpret_cast<uint8_t*>(sLut);
+        for (int e = threadIdx.x - 64; e < kLutEntries; e += 64) {
+            const int s = e >> 4, u = e & 15;
+            const float v = (float)(u < 8 ? u : u - 16);
+            lut[e] = (uint8_t)e4m3_rn(__fmul_rn(v, e4m3_decode((uint32_t)s)));
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = misc[0];
+
+    SegIter it;
+    int tile, g0, g1;
+
+    if (warp == 0) {
+        // ------------------------------------------------------- TMA producer
+        if (lane == 0) {
+            const uint64_t pol_w = ptx::policy_evict_first();   // weights: streamed once
+            const uint64_t pol_x = ptx::policy_evict_last();    // activations: re-read by every tile
+            it.init(a, blockIdx.x);
+            int i = 0;
+            while (it.next(tile, g0, g1)) {
+                const int ntile = tile % a.n_tiles, mtile = tile / a.n_tiles;
+                for (int g = g0; g < g1; ++g, ++i) {
+                    const int s = i % STAGES;
+                    ptx::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+                    ptx::mbar_arrive_expect_tx(&full[s], C::kStageTx);
+                    const size_t blk = (size_t)ntile * a.G + g;
+                    ptx::bulk_g2s(sW + s * kWBytes, a.w_packed + blk * kWBytes, kWBytes, &full[s], pol_w);
+                    ptx::bulk_g2s(sS + s * kTileN, a.w_scales + blk * kTileN, kTileN, &full[s], pol_w);
+                    ptx::tma_2d_g2s(sX + s * C::kXBytes, &tmap_x, g * kGroup, mtile * NTOK, &full[s], pol_x);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ------------------------------------------------------- MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc_pos = make_idesc(NTOK, false);
+            constexpr uint32_t idesc_neg = make_idesc(NTOK, true);
+            it.init(a, blockIdx.x);
+            int i = 0, sg = 0;
+            while (it.next(tile, g0, g1)) {
+                const int b = sg % ACCBUF;
+                ptx::mbar_wait(&accempty[b], ((sg / ACCBUF) & 1) ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem + b * NTOK;
+                uint32_t acc = 0;
+                for (int g = g0; g < g1; ++g, ++i) {
+                    const int s = i % STAGES, as = i % ASTAGES;
+                    ptx::mbar_wait(&afull[as], (i / ASTAGES) & 1);
+                    ptx::mbar_wait(&full[s], (i / STAGES) & 1);
+                    ptx::tc_fence_after();
+                    const uint32_t ta = tmem + C::kACol0 + as * C::kASz;
+                    const uint64_t bdesc = smem_desc_sw128(ptx::smem_u32(sX + s * C::kXBytes));
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint64_t bd = bdesc + (uint64_t)(j * 32 >> 4);   // +32 B along K
+                        ptx::mma_f8f6f4_ts(d, ta + j * 8, bd, idesc_pos, acc);
+                        acc = 1;
+                        if (SIGN_SPLIT) ptx::mma_f8f6f4_ts(d, ta + 32 + j * 8, bd, idesc_neg, 1);
+                    }
+                    ptx::mma_commit(&empty[s]);
+                    ptx::mma_commit(&aempty[as]);
+                }
+                ptx::mma_commit(&accfull[b]);
+                ++sg;
+            }
+        }
+        __syncwarp();
+    } else if (warp >= 8) {
+        // ------------------------------------------------------- converters
+        const int wg = (warp - 8) >> 2;           // converter warpgroup
+        const int r = threadIdx.x & 127;          // weight row == TMEM lane
+        const uint32_t lane_base = (uint32_t)(r & ~31) << 16;
+        it.init(a, blockIdx.x);
+        int i = 0;
+        while (it.next(tile, g0, g1)) {
+            for (int g = g0; g < g1; ++g, ++i) {
+                if ((i % NCONV) != wg) continue;
+                const int s = i % STAGES, as = i % ASTAGES;
+                ptx::mbar_wait(&full[s], (i / STAGES) & 1);
+                ptx::mbar_wait(&aempty[as], ((i / ASTAGES) & 1) ^ 1);
+                ptx::tc_fence_after();
+                const uint4 L = sLut[sS[s * kTileN + r]];
+                const uint8_t* wrow = sW + s * kWBytes + r * 16;
+                const uint32_t ta = tmem + lane_base + C::kACol0 + as * C::kASz;
+                if (SIGN_SPLIT) {
+                    const uint32_t N0 = L.z & 0x7F7F7F7Fu, N1 = L.w & 0x7F7F7F7Fu;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint4 wv = *reinterpret_cast<const uint4*>(wrow + j * 128 * 16);
+                        uint32_t P[8], Q[8];
+                        conv_sign_split(wv.x, L.x, L.y, N0, N1, P[0], P[1], Q[0], Q[1]);
+                        conv_sign_split(wv.y, L.x, L.y, N0, N1, P[2], P[3], Q[2], Q[3]);
+                        conv_sign_split(wv.z, L.x, L.y, N0, N1, P[4], P[5], Q[4], Q[5]);
+                        conv_sign_split(wv.w, L.x, L.y, N0, N1, P[6], P[7], Q[6], Q[7]);
+                        ptx::tmem_st_x8(ta + j * 8, P);
+                        ptx::tmem_st_x8(ta + 32 + j * 8, Q);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint4 wv = *reinterpret_cast<const uint4*>(wrow + j * 128 * 16);
+                        uint32_t R[8];
+                        conv_mask_select(wv.x, L.x, L.y, L.z, L.w, R[0], R[1]);
+                        conv_mask_select(wv.y, L.x, L.y, L.z, L.w, R[2], R[3]);
+                        conv_mask_select(wv.z, L.x, L.y, L.z, L.w, R[4], R[5]);
+                        conv_mask_select(wv.w, L.x, L.y, L.z, L.w, R[6], R[7]);
+                        ptx::tmem_st_x8(ta + j * 8, R);
+                    }
+                }
+                ptx::tmem_wait_st();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&afull[as]);
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------------- epilogue
+        const int r = threadIdx.x & 127;
+        const uint32_t lane_base = (uint32_t)(r & ~31) << 16;
+        const float p2 = exp2_neg(a.pts_n);
+        it.init(a, blockIdx.x);
+        int sg = 0;
+        const long long u_first = (long long)blockIdx.x * a.U / a.C;
+        while (it.next(tile, g0, g1)) {
+            const int b = sg % ACCBUF;
+            ptx::mbar_wait(&accfull[b], (sg / ACCBUF) & 1);
+            ptx::tc_fence_after();
+            const int ntile = tile % a.n_tiles, mtile = tile / a.n_tiles;
+            const int n = ntile * kTileN + r;
+            const int m0 = mtile * NTOK;
+            const bool whole = (g0 == 0 && g1 == a.G);
+            int slot = 0;
+            if (!whole) slot = 2 * blockIdx.x + ((u_first < (long long)tile * a.G) ? 1 : 0);   // first/last segment
+            const float gam = a.gamma ? a.gamma[n] : 1.0f;
+            float* part = a.partial + (size_t)slot * NTOK * kTileN;
+#pragma unroll 1
+            for (int ch = 0; ch < NTOK / 16; ++ch) {
+                uint32_t v[16];
+                ptx::tmem_ld_x16(tmem + lane_base + b * NTOK + ch * 16, v);
+                ptx::tmem_wait_ld();
+                if (whole) {
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        const int m = m0 + ch * 16 + c;
+                        if (m < a.M) {
+                            float y = __fmul_rn(__uint_as_float(v[c]), __fmul_rn(__bfloat162float(a.x_scale[m]), p2));
+                            if (a.gamma) y = __fmul_rn(y, gam);
+                            const __nv_bfloat16 yb = __float2bfloat16_rn(y);
+                            if (a.out_layout == 0) a.Y[(size_t)m * a.ldy + n] = yb;
+                            else a.Y[(size_t)n * a.ldy + m] = yb;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) part[(ch * 16 + c) * kTileN + r] = __uint_as_float(v[c]);
+                }
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&accempty[b]);
+            if (!whole) {
+                // deterministic cross-CTA reduction: last arriver sums contributors in CTA order
+                __threadfence();
+                ptx::named_bar_sync(1, 128);
+                const long long t0 = (long long)tile * a.G, t1 = t0 + a.G - 1;
+                const int c_lo = owner_of(t0, a.U, a.C), c_hi = owner_of(t1, a.U, a.C);
+                if (r == 0) {
+                    const unsigned prev = atomicAdd(&a.counters[tile], 1u);
+                    misc[1] = (prev == (unsigned)(c_hi - c_lo)) ? 1u : 0u;
+                }
+                ptx::named_bar_sync(1, 128);
+                if (misc[1]) {
+                    __threadfence();
+#pragma unroll 1
+                    for (int ch = 0; ch < NTOK / 16; ++ch) {
+                        float accv[16];
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) accv[c] = 0.0f;
+                        for (int cc = c_lo; cc <= c_hi; ++cc) {
+                            const long long cu0 = (long long)cc * a.U / a.C;
+                            const int sl = 2 * cc + ((cu0 < t0) ? 1 : 0);
+                            const float* pp = a.partial + (size_t)sl * NTOK * kTileN;
+#pragma unroll
+                            for (int c = 0; c < 16; ++c)
+                                accv[c] = __fadd_rn(accv[c], __ldcg(pp + (ch * 16 + c) * kTileN + r));
+                        }
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) {
+                            const int m = m0 + ch * 16 + c;
+                            if (m < a.M) {
+                                float y = __fmul_rn(accv[c], __fmul_rn(__bfloat162float(a.x_scale[m]), p2));
+                                if (a.gamma) y = __fmul_rn(y, gam);
+                                const __nv_bfloat16 yb = __float2bfloat16_rn(y);
+                                if (a.out_layout == 0) a.Y[(size_t)m * a.ldy + n] = yb;
+                                else a.Y[(size_t)n * a.ldy + m] = yb;
+                            }
+                        }
+                    }
+                    if (r == 0) a.counters[tile] = 0u;   // leave the workspace zeroed
+                }
+                ptx::named_bar_sync(1, 128);
+            }
+            ++sg;
+        }
+    }
+
+    // ------------------------------------------------------------ teardown
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (warp == 2) ptx::tmem_dealloc(tmem, C::kTmemCols);
+}
+
+__global__ void k_lut_table(uint8_t* out) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kLutEntries; e += gridDim.x * blockDim.x) {
+        const int s = e >> 4, u = e & 15;
+        const float v = (float)(u < 8 ? u : u - 16);
+        out[e] = (uint8_t)e4m3_rn(__fmul_rn(v, e4m3_decode((uint32_t)s)));
+    }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(p);
+    });
+    return fn;
+}
+
+// TMA descriptor cache keyed by (pointer, M, K, box rows).
+bool make_x_map(CUtensorMap* out, const uint8_t* x, int64_t M, int64_t K, int ntok) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int64_t, int64_t, int>, CUtensorMap> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_tuple((const void*)x, M, K, ntok);
+    auto itc = cache.find(key);
+    if (itc != cache.end()) { *out = itc->second; return true; }
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
+    cuuint64_t strides[1] = {(cuuint64_t)K};
+    cuuint32_t box[2] = {(cuuint32_t)kGroup, (cuuint32_t)ntok};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(x), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    if (cache.size() > 4096) cache.clear();
+    cache[key] = *out;
+    return true;
+}
+
+struct Plan {
+    int ntok, m_tiles, n_tiles, tiles, G, mode, C;
+    long long U;
+    bool sign_split;
+};
+
+Plan make_plan(int64_t M, int64_t N, int64_t K) {
+    Plan p{};
+    p.ntok = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
+    p.sign_split = p.ntok <= 128;
+    p.m_tiles = (int)((M + p.ntok - 1) / p.ntok);
+    p.n_tiles = (int)(N / kTileN);
+    p.tiles = p.m_tiles * p.n_tiles;
+    p.G = (int)(K / kGroup);
+    const int sms = sm_count();
+    if (p.tiles >= 2 * sms) {
+        p.mode = 0;
+        p.C = sms;
+        p.U = (long long)p.tiles * p.G;
+    } else {
+        p.mode = 1;
+        p.U = (long long)p.tiles * p.G;
+        p.C = (int)std::min<long long>(sms, p.U);
+    }
+    return p;
+}
+
+template <int NTOK, bool SS, int NCONV, int STAGES, int ASTAGES, int ACCBUF>
+fireq_status_t launch_cfg(const CUtensorMap& map, const GemmArgs& args, cudaStream_t stream) {
+    using C = Cfg<NTOK, SS, NCONV, STAGES, ASTAGES, ACCBUF>;
+    auto kern = k_w4a8_gemm<NTOK, SS, NCONV, STAGES, ASTAGES, ACCBUF>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
+            return fail(FIREQ_ERROR_CUDA, "cudaFuncSetAttribute(smem) failed");
+        attr_done = true;
+    }
+    kern<<<args.C, C::kThreads, C::kSmemBytes, stream>>>(map, args);
+    return check_launch("fireq_w4a8_gemm");
+}
+
+}  // namespace
+
+size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
+    const Plan p = make_plan(M, N, K);
+    const size_t part = p.mode == 1 ? (size_t)2 * p.C * p.ntok * kTileN * sizeof(float) : 0;
+    const size_t cnt = ((size_t)p.tiles * sizeof(unsigned) + 255) / 256 * 256;
+    return cnt + part;
+}
+
+fireq_status_t gemm_plan(int64_t M, int64_t N, int64_t K, int32_t* cfg) {
+    const Plan p = make_plan(M, N, K);
+    cfg[0] = p.ntok;
+    cfg[1] = p.mode;
+    cfg[2] = p.C;
+    cfg[3] = p.sign_split ? 1 : 0;
+    return FIREQ_SUCCESS;
+}
+
+fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int64_t M, int64_t K,
+                         const uint8_t* w_packed, const uint8_t* w_scales, int64_t N, int32_t pts_n,
+                         const float* gamma, __nv_bfloat16* Y, int64_t ldy, int out_layout, void* ws,
+                         size_t ws_bytes, cudaStream_t stream) {
+    const Plan p = make_plan(M, N, K);
+    if (ws_bytes < gemm_workspace_bytes(M, N, K)) return fail(FIREQ_ERROR_WORKSPACE, "GEMM workspace too small");
+    CUtensorMap map;
+    if (!make_x_map(&map, x_fp8, M, K, p.ntok)) return fail(FIREQ_ERROR_CUDA, "cuTensorMapEncodeTiled failed");
+    GemmArgs args{};
+    args.w_packed = w_packed;
+    args.w_scales = w_scales;
+    args.x_scale = x_scale;
+    args.gamma = gamma;
+    args.Y = Y;
+    const size_t cnt = ((size_t)p.tiles * sizeof(unsigned) + 255) / 256 * 256;
+    args.counters = static_cast<unsigned*>(ws);
+    args.partial = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + cnt);
+    args.ldy = ldy;
+    args.M = (int)M; args.N = (int)N; args.K = (int)K; args.G = p.G;
+    args.n_tiles = p.n_tiles; args.m_tiles = p.m_tiles; args.tiles = p.tiles;
+    args.pts_n = pts_n;
+    args.out_layout = out_layout;
+    args.mode = p.mode;
+    args.C = p.C;
+    args.U = p.U;
+    switch (p.ntok) {
+        case 16:  return launch_cfg<16, true, 2, 16, 4, 2>(map, args, stream);
+        case 32:  return launch_cfg<32, true, 2, 14, 4, 2>(map, args, stream);
+        case 64:  return launch_cfg<64, true, 2, 10, 4, 2>(map, args, stream);
+        case 128: return launch_cfg<128, true, 2, 7, 4, 2>(map, args, stream);
+        default:  return launch_cfg<256, false, 2, 4, 4, 1>(map, args, stream);
+    }
+}
+
+fireq_status_t debug_lut_table(uint8_t* out, cudaStream_t stream) {
+    k_lut_table<<<8, 256, 0, stream>>>(out);
+    return check_launch("fireq_debug_lut_table");
+}
+
+}  // namespace fireq

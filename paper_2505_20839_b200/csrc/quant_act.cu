@@ -1,0 +1,101 @@
+// quant_act.cu -- fireq_quantize_act (A1..A3, Eq. 2, per token P:482) and the
+// FFN helper fireq_silu_mul_quantize_act (SiLU * up, then A2..A3).
+//
+// One CTA per token row; the row is read twice (amax pass, encode pass; the second
+// pass hits L1/L2).  Memory-bound: 2 B read + 1 B written per element.
+#include "common.cuh"
+
+namespace fireq {
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ float block_max(float v, float* red) {
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = l < (kThreads / 32) ? red[l] : 0.0f;
+        for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (l == 0) red[0] = v;
+    }
+    __syncthreads();
+    return red[0];
+}
+
+// x' for 8 consecutive elements (A1): bf16(x * c) when c is given (product exact in fp32).
+struct Src {
+    const __nv_bfloat16* X;
+    const __nv_bfloat16* U;   // silu-mul mode: X = gate, U = up
+    const __nv_bfloat16* c;
+    int mode;                 // 0 = plain, 1 = channel multiplier, 2 = silu(g) * u
+};
+
+__device__ __forceinline__ void load8(const Src& s, int64_t row_off, int64_t k, float (&v)[8]) {
+    const uint4 rx = *reinterpret_cast<const uint4*>(s.X + row_off + k);
+    const __nv_bfloat16* hx = reinterpret_cast<const __nv_bfloat16*>(&rx);
+    if (s.mode == 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = __bfloat162float(hx[i]);
+    } else if (s.mode == 1) {
+        const uint4 rc = *reinterpret_cast<const uint4*>(s.c + k);
+        const __nv_bfloat16* hc = reinterpret_cast<const __nv_bfloat16*>(&rc);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            v[i] = __bfloat162float(__float2bfloat16_rn(__fmul_rn(__bfloat162float(hx[i]), __bfloat162float(hc[i]))));
+    } else {
+        const uint4 ru = *reinterpret_cast<const uint4*>(s.U + row_off + k);
+        const __nv_bfloat16* hu = reinterpret_cast<const __nv_bfloat16*>(&ru);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float g = __bfloat162float(hx[i]);
+            const float silu = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
+            v[i] = __bfloat162float(__float2bfloat16_rn(__fmul_rn(silu, __bfloat162float(hu[i]))));
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_act_quant(Src s, int64_t K, int64_t ld,
+                                                        uint8_t* __restrict__ xq,
+                                                        __nv_bfloat16* __restrict__ beta_out) {
+    __shared__ float red[32];
+    const int64_t m = blockIdx.x;
+    const int64_t row_off = m * ld;
+    float amax = 0.0f;
+    for (int64_t k = (int64_t)threadIdx.x * 8; k < K; k += kThreads * 8) {
+        float v[8];
+        load8(s, row_off, k, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) amax = fmaxf(amax, fabsf(v[i]));
+    }
+    amax = block_max(amax, red);
+    // A2: beta = bf16_RN(amax / 448) (fp32 division then RNE; equals exact RNE for bf16 operands)
+    const __nv_bfloat16 beta_h = amax > 0.0f ? __float2bfloat16_rn(__fdiv_rn(amax, 448.0f))
+                                             : __float2bfloat16_rn(1.0f);
+    const float beta = __bfloat162float(beta_h);
+    if (threadIdx.x == 0) beta_out[m] = beta_h;
+    // A3: x_hat = E4M3_RN_satfinite(x' / beta)
+    for (int64_t k = (int64_t)threadIdx.x * 8; k < K; k += kThreads * 8) {
+        float v[8];
+        load8(s, row_off, k, v);
+        uint2 o;
+        o.x = e4m3x2_rn(__fdiv_rn(v[0], beta), __fdiv_rn(v[1], beta)) |
+              (e4m3x2_rn(__fdiv_rn(v[2], beta), __fdiv_rn(v[3], beta)) << 16);
+        o.y = e4m3x2_rn(__fdiv_rn(v[4], beta), __fdiv_rn(v[5], beta)) |
+              (e4m3x2_rn(__fdiv_rn(v[6], beta), __fdiv_rn(v[7], beta)) << 16);
+        *reinterpret_cast<uint2*>(xq + m * K + k) = o;
+    }
+}
+
+}  // namespace
+
+fireq_status_t quantize_act_impl(const __nv_bfloat16* X, const __nv_bfloat16* U, int64_t M, int64_t K,
+                                 int64_t ld, const __nv_bfloat16* c, int mode, uint8_t* xq,
+                                 __nv_bfloat16* beta, cudaStream_t stream) {
+    Src s{X, U, c, mode};
+    k_act_quant<<<(unsigned)M, kThreads, 0, stream>>>(s, K, ld, xq, beta);
+    return check_launch(mode == 2 ? "fireq_silu_mul_quantize_act" : "fireq_quantize_act");
+}
+
+}  // namespace fireq

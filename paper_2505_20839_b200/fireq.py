@@ -1,0 +1,244 @@
+"""Thin ctypes binding of libfireq.so (include/fireq.h) -- argument marshalling only.
+
+Every step of the FireQ path runs in the library's CUDA kernels; this module only
+turns torch CUDA tensors into device pointers + the current CUDA stream and maps
+status codes to exceptions.  There is no CPU or PyTorch fallback: if the library
+is missing, or a tensor is not on a CUDA device, the call raises.
+"""
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfireq.so")
+
+_lib = None
+
+EXPORTS = [
+    "fireq_status_string", "fireq_last_error", "fireq_weight_layout_version",
+    "fireq_packed_weight_bytes", "fireq_weight_scale_bytes",
+    "fireq_quantize_weight_workspace_bytes", "fireq_w4a8_gemm_workspace_bytes",
+    "fireq_quantize_weight", "fireq_quantize_act", "fireq_silu_mul_quantize_act",
+    "fireq_w4a8_gemm", "fireq_comm_get_unique_id", "fireq_comm_init", "fireq_comm_destroy",
+    "fireq_w4a8_gemm_colpar", "fireq_debug_lut_table", "fireq_gemm_plan",
+]
+
+
+class FireqError(RuntimeError):
+    pass
+
+
+def load(path=LIB_PATH):
+    """Load libfireq.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise FireqError(f"libfireq.so not found at {path}: run __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
+    P, I64, I32, SZ, C = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t, ctypes.c_int
+    sig = {
+        "fireq_status_string": ([C], ctypes.c_char_p),
+        "fireq_last_error": ([], ctypes.c_char_p),
+        "fireq_weight_layout_version": ([], C),
+        "fireq_packed_weight_bytes": ([I64, I64], SZ),
+        "fireq_weight_scale_bytes": ([I64, I64], SZ),
+        "fireq_quantize_weight_workspace_bytes": ([I64, I64], SZ),
+        "fireq_w4a8_gemm_workspace_bytes": ([I64, I64, I64], SZ),
+        "fireq_quantize_weight": ([P, I64, I64, C, P, P, P, P, P, P, SZ, P], C),
+        "fireq_quantize_act": ([P, I64, I64, I64, P, P, P, P], C),
+        "fireq_silu_mul_quantize_act": ([P, P, I64, I64, I64, P, P, P], C),
+        "fireq_w4a8_gemm": ([P, P, I64, I64, P, P, I64, I32, P, P, I64, C, P, SZ, P], C),
+        "fireq_comm_get_unique_id": ([P], C),
+        "fireq_comm_init": ([P, C, C, P], C),
+        "fireq_comm_destroy": ([P], C),
+        "fireq_w4a8_gemm_colpar": ([P, P, I64, I64, P, P, I64, I32, P, P, SZ, P, P], C),
+        "fireq_debug_lut_table": ([P, P], C),
+        "fireq_gemm_plan": ([I64, I64, I64, P], C),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = lib
+    return lib
+
+
+def lib():
+    return load()
+
+
+def _check(status, what):
+    if status != 0:
+        L = lib()
+        raise FireqError(f"{what}: {L.fireq_status_string(status).decode()}: {L.fireq_last_error().decode()}")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise FireqError("fireq: tensors must live on a CUDA device (no CPU path)")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+# ------------------------------------------------------------------- sizes
+def packed_weight_bytes(N, K):
+    return lib().fireq_packed_weight_bytes(N, K)
+
+
+def weight_scale_bytes(N, K):
+    return lib().fireq_weight_scale_bytes(N, K)
+
+
+def gemm_workspace_bytes(M, N, K):
+    return lib().fireq_w4a8_gemm_workspace_bytes(M, N, K)
+
+
+def layout_version():
+    return lib().fireq_weight_layout_version()
+
+
+def gemm_plan(M, N, K):
+    cfg = (ctypes.c_int32 * 4)()
+    _check(lib().fireq_gemm_plan(M, N, K, ctypes.cast(cfg, ctypes.c_void_p)), "fireq_gemm_plan")
+    return {"ntok": cfg[0], "mode": "stream-k" if cfg[1] else "tiles", "ctas": cfg[2], "sign_split": bool(cfg[3])}
+
+
+# ------------------------------------------------------------------- calls
+class QuantizedWeight:
+    """Device tensors produced by fireq_quantize_weight."""
+
+    def __init__(self, packed, scales, lam, c, pts_and_status, N, K):
+        self.packed, self.scales, self.lam, self.c = packed, scales, lam, c
+        self.pts_and_status = pts_and_status
+        self.N, self.K = N, K
+        self._n = None
+
+    @property
+    def n(self):
+        """PTS exponent (reads the device scalar back once, as the C ABI prescribes)."""
+        if self._n is None:
+            host = self.pts_and_status.cpu()
+            if int(host[1]) != 0:
+                raise FireqError(f"fireq_quantize_weight device status {int(host[1])}")
+            self._n = int(host[0])
+        return self._n
+
+
+def quantize_weight(W, cas_mode=1, stream=None, out=None):
+    """W: bf16 [N][K] CUDA tensor -> QuantizedWeight (all device tensors)."""
+    assert W.dtype == torch.bfloat16 and W.dim() == 2 and W.is_contiguous()
+    N, K = W.shape
+    dev = W.device
+    L = lib()
+    if out is None:
+        packed = torch.empty(L.fireq_packed_weight_bytes(N, K), dtype=torch.uint8, device=dev)
+        scales = torch.empty(L.fireq_weight_scale_bytes(N, K), dtype=torch.uint8, device=dev)
+    else:
+        packed, scales = out
+    lam = torch.empty(K, dtype=torch.float32, device=dev)
+    c = torch.empty(K, dtype=torch.bfloat16, device=dev)
+    ps = torch.empty(2, dtype=torch.int32, device=dev)
+    ws = torch.empty(L.fireq_quantize_weight_workspace_bytes(N, K), dtype=torch.uint8, device=dev)
+    _check(L.fireq_quantize_weight(_ptr(W), N, K, cas_mode, _ptr(packed), _ptr(scales), _ptr(lam), _ptr(c),
+                                   _ptr(ps), _ptr(ws), ws.numel(), _stream(stream)), "fireq_quantize_weight")
+    return QuantizedWeight(packed, scales, lam, c, ps, N, K)
+
+
+def quantize_act(X, chan_mul=None, stream=None, out=None):
+    """X: bf16 [M][ld] -> (x_fp8 uint8 [M][K], beta bf16 [M]).  K = X.shape[1]."""
+    assert X.dtype == torch.bfloat16 and X.dim() == 2 and X.stride(1) == 1
+    M, K = X.shape
+    if out is None:
+        xq = torch.empty((M, K), dtype=torch.uint8, device=X.device)
+        beta = torch.empty(M, dtype=torch.bfloat16, device=X.device)
+    else:
+        xq, beta = out
+    _check(lib().fireq_quantize_act(_ptr(X), M, K, X.stride(0), _ptr(chan_mul), _ptr(xq), _ptr(beta),
+                                    _stream(stream)), "fireq_quantize_act")
+    return xq, beta
+
+
+def silu_mul_quantize_act(G, U, stream=None, out=None):
+    assert G.shape == U.shape and G.stride() == U.stride()
+    M, K = G.shape
+    if out is None:
+        xq = torch.empty((M, K), dtype=torch.uint8, device=G.device)
+        beta = torch.empty(M, dtype=torch.bfloat16, device=G.device)
+    else:
+        xq, beta = out
+    _check(lib().fireq_silu_mul_quantize_act(_ptr(G), _ptr(U), M, K, G.stride(0), _ptr(xq), _ptr(beta),
+                                             _stream(stream)), "fireq_silu_mul_quantize_act")
+    return xq, beta
+
+
+class Workspace:
+    """Zero-initialised GEMM workspace (the counters must start at zero, fireq.h)."""
+
+    def __init__(self, nbytes, device="cuda"):
+        self.t = torch.zeros(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+    def ensure(self, nbytes):
+        if self.t.numel() < nbytes:
+            self.t = torch.zeros(int(nbytes), dtype=torch.uint8, device=self.t.device)
+        return self.t
+
+
+def w4a8_gemm(xq, beta, packed, scales, N, pts_n, gamma=None, out=None, out_layout=0, workspace=None,
+              stream=None):
+    """Y = fireq_w4a8_gemm(...): bf16 [M][N] (out_layout 0) or [N][M] (out_layout 1)."""
+    M, K = xq.shape
+    L = lib()
+    need = L.fireq_w4a8_gemm_workspace_bytes(M, N, K)
+    ws = workspace.ensure(need) if workspace is not None else torch.zeros(need, dtype=torch.uint8, device=xq.device)
+    if out is None:
+        out = torch.empty((M, N) if out_layout == 0 else (N, M), dtype=torch.bfloat16, device=xq.device)
+    ldy = out.stride(0)
+    _check(L.fireq_w4a8_gemm(_ptr(xq), _ptr(beta), M, K, _ptr(packed), _ptr(scales), N, pts_n, _ptr(gamma),
+                             _ptr(out), ldy, out_layout, _ptr(ws), ws.numel(), _stream(stream)), "fireq_w4a8_gemm")
+    return out
+
+
+def debug_lut_table(device="cuda"):
+    out = torch.empty(127 * 16, dtype=torch.uint8, device=device)
+    _check(lib().fireq_debug_lut_table(_ptr(out), _stream()), "fireq_debug_lut_table")
+    return out
+
+
+# --------------------------------------------------------------- multi-GPU
+class Comm:
+    """NCCL communicator wrapper (fireq_comm_t)."""
+
+    def __init__(self, nranks, rank, uid_bytes):
+        self.h = ctypes.c_void_p()
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(bytes(uid_bytes))
+        _check(lib().fireq_comm_init(ctypes.byref(self.h), nranks, rank, ctypes.cast(buf, ctypes.c_void_p)),
+               "fireq_comm_init")
+        self.nranks, self.rank = nranks, rank
+
+    @staticmethod
+    def unique_id():
+        buf = (ctypes.c_uint8 * 128)()
+        _check(lib().fireq_comm_get_unique_id(ctypes.cast(buf, ctypes.c_void_p)), "fireq_comm_get_unique_id")
+        return bytes(buf)
+
+    def destroy(self):
+        if self.h:
+            _check(lib().fireq_comm_destroy(self.h), "fireq_comm_destroy")
+            self.h = ctypes.c_void_p()
+
+
+def w4a8_gemm_colpar(xq, beta, packed_local, scales_local, N_local, pts_n, comm, Yt_full, workspace, stream=None):
+    M, K = xq.shape
+    ws = workspace.ensure(lib().fireq_w4a8_gemm_workspace_bytes(M, N_local, K))
+    _check(lib().fireq_w4a8_gemm_colpar(_ptr(xq), _ptr(beta), M, K, _ptr(packed_local), _ptr(scales_local), N_local,
+                                        pts_n, _ptr(Yt_full), _ptr(ws), ws.numel(), comm.h, _stream(stream)),
+           "fireq_w4a8_gemm_colpar")
+    return Yt_full

@@ -1,0 +1,252 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Quantization, packing, LUT and activation encoding must match bit-exactly; the
+GEMM must satisfy the G4 criterion (max |y - r| / max(|r|, 0.1 rms_row(r)) <= 1e-2,
+DESIGN.md "Tolerance") against the oracle's fp64 reference, and be bit-exact on
+the exactness corridor.  All inputs are seeded synthetic (synth/).
+"""
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import gemm as og
+from oracle import layout as ol
+from oracle import numerics as nm
+from oracle import quant as oq
+
+pytestmark = pytest.mark.gpu
+
+G4_TOL = 1e-2
+DEV = "cuda"
+
+
+def to_dev_bf16(bits):
+    return synth.bits_to_torch(bits).to(DEV)
+
+
+def bits_of(t):
+    return t.cpu().view(torch.int16).numpy().view(np.uint16)
+
+
+# ----------------------------------------------------------------- LUT
+def test_lut_table_bit_exact(fireq):
+    got = fireq.debug_lut_table().cpu().numpy().reshape(127, 16)
+    assert np.array_equal(got, og.lut_of_luts())
+
+
+# ------------------------------------------------------- weight quantizer
+def check_weight(fireq, wbits, cas_mode):
+    N, K = wbits.shape
+    qw = fireq.quantize_weight(to_dev_bf16(wbits), cas_mode=cas_mode)
+    torch.cuda.synchronize()
+    ref = oq.quantize_weight(synth.bits_to_f64(wbits), cas_mode)
+    ps = qw.pts_and_status.cpu().numpy()
+    assert ps[1] == 0 and ps[0] == ref.n
+    assert np.array_equal(qw.lam.cpu().numpy().astype(np.float64), ref.lam)
+    assert np.array_equal(bits_of(qw.c), nm.bf16_to_bits(ref.c))
+    assert np.array_equal(qw.scales.cpu().numpy(), ref.scales)
+    assert np.array_equal(qw.packed.cpu().numpy(), ref.packed)
+    return qw, ref
+
+
+@pytest.mark.parametrize("N,K,cas", [(128, 128, 0), (256, 512, 1), (384, 1280, 1), (1024, 4096, 0), (4096, 4096, 1)])
+def test_quantize_weight_synthetic(fireq, N, K, cas):
+    check_weight(fireq, synth.weights(N, K, synth.layer_seed(1, N + K)), cas)
+
+
+def test_quantize_weight_f_edge(fireq):
+    import json, os
+    from fractions import Fraction
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "f_edge.json")))
+    K = 128 * g["K_groups"]
+    W = np.zeros((128, K))
+    for i, row in enumerate(g["rows"]):
+        W[i, :len(row["values"])] = [float(Fraction(v)) for v in row["values"]]
+    qw, ref = check_weight(fireq, nm.bf16_to_bits(W), g["cas_mode"])
+    assert ref.n == g["pts_n"]
+
+
+@pytest.mark.parametrize("case", ["band224", "band448", "tiny", "ones", "neg_near_max", "zero_cols", "subnormal"])
+def test_quantize_weight_edges(fireq, case):
+    rng = np.random.default_rng(zlib.crc32(case.encode()))
+    W = nm.bf16_rn(rng.standard_normal((256, 384)) * 0.02)
+    if case == "band224":
+        W[3, 7] = 224.0
+    elif case == "band448":
+        W[5, 9] = 448.0
+        W[6, 1] = -447.0
+    elif case == "tiny":
+        W = nm.bf16_rn(W * 2.0 ** -30)
+    elif case == "ones":
+        W = np.ones_like(W)
+    elif case == "neg_near_max":
+        W[:, ::128] = -np.abs(W).max() * 1.01
+        W = nm.bf16_rn(W)
+    elif case == "zero_cols":
+        W[:, 5:40] = 0.0
+    elif case == "subnormal":
+        W[0, 0] = 2.0 ** -130
+        W = nm.bf16_rn(W)
+    W = nm.bf16_rn(W)
+    for cas in (0, 1):
+        check_weight(fireq, nm.bf16_to_bits(W), cas)
+
+
+def test_quantize_weight_nonfinite_status(fireq):
+    W = np.ones((128, 128))
+    bits = nm.bf16_to_bits(W)
+    bits[3, 3] = 0x7FC0          # NaN
+    qw = fireq.quantize_weight(to_dev_bf16(bits), cas_mode=0)
+    assert int(qw.pts_and_status.cpu()[1]) == 1   # FIREQ_ERROR_INVALID_VALUE
+
+
+# ---------------------------------------------------- activation quantizer
+@pytest.mark.parametrize("M,K,with_c", [(1, 128, False), (16, 4096, True), (17, 11008, False), (300, 1024, True),
+                                        (5, 14336, True)])
+def test_quantize_act(fireq, M, K, with_c):
+    xb = synth.activations(M, K, synth.layer_seed(2, M * 7 + K))
+    X = synth.bits_to_f64(xb)
+    X[0, :5] = [0.0, -0.0, 1e-30, -2.0 ** -130, 0.0]
+    xb = nm.bf16_to_bits(nm.bf16_rn(X))
+    if M > 2:
+        xb[2, :] = 0                                # all-zero row -> beta = 1
+    X = synth.bits_to_f64(xb)
+    c = None
+    cb = None
+    if with_c:
+        c = nm.bf16_rn(np.exp(np.random.default_rng(K).normal(0, 0.5, K)))
+        cb = to_dev_bf16(nm.bf16_to_bits(c))
+    xq, beta = fireq.quantize_act(to_dev_bf16(xb), chan_mul=cb)
+    rq, rbeta = oq.quantize_act(X, c)
+    assert np.array_equal(bits_of(beta), nm.bf16_to_bits(rbeta))
+    assert np.array_equal(xq.cpu().numpy(), rq)
+
+
+def test_quantize_act_strided(fireq):
+    M, K, ld = 8, 256, 384
+    xb = synth.activations(M, ld, 77)
+    Xd = to_dev_bf16(xb)[:, :K]
+    xq, beta = fireq.quantize_act(Xd)
+    rq, rbeta = oq.quantize_act(synth.bits_to_f64(xb)[:, :K])
+    assert np.array_equal(xq.cpu().numpy(), rq)
+
+
+# ----------------------------------------------------------------- GEMM
+def run_case(fireq, M, N, K, cas=1, gamma=False, out_layout=0, seed=0):
+    wb = synth.weights(N, K, synth.layer_seed(3, seed))
+    xb = synth.activations(M, K, synth.layer_seed(4, seed))
+    qw = fireq.quantize_weight(to_dev_bf16(wb), cas_mode=cas)
+    xq, beta = fireq.quantize_act(to_dev_bf16(xb), chan_mul=qw.c)
+    gam = None
+    g_np = None
+    if gamma:
+        g_np = nm.f32(np.random.default_rng(seed).uniform(0.5, 2.0, N))
+        gam = torch.from_numpy(g_np.astype(np.float32)).to(DEV)
+    Y = fireq.w4a8_gemm(xq, beta, qw.packed, qw.scales, N, qw.n, gamma=gam, out_layout=out_layout)
+    torch.cuda.synchronize()
+    y = Y.float().cpu().numpy().astype(np.float64)
+    if out_layout == 1:
+        y = y.T
+    # oracle reference from the oracle's own quantization of the same inputs
+    ref = oq.quantize_weight(synth.bits_to_f64(wb), cas)
+    rq, rbeta = oq.quantize_act(synth.bits_to_f64(xb), ref.c)
+    assert np.array_equal(qw.packed.cpu().numpy(), ref.packed)
+    assert np.array_equal(xq.cpu().numpy(), rq)
+    r = og.gemm_reference(rq, rbeta, ref.packed, ref.scales, N, K, ref.n, gamma=g_np)
+    return y, r, qw, xq, beta
+
+
+@pytest.mark.parametrize("M,N,K", [
+    (1, 128, 128), (7, 256, 512), (16, 512, 1024), (16, 1024, 4096), (17, 384, 640), (32, 256, 2048),
+    (64, 640, 1024), (100, 256, 768), (128, 512, 512), (129, 256, 1024), (256, 384, 512), (300, 256, 384),
+    (513, 128, 256),
+])
+def test_gemm_g4(fireq, M, N, K):
+    y, r, *_ = run_case(fireq, M, N, K, seed=M * 131 + N + K)
+    err = og.g4_error(y, r)
+    assert err <= G4_TOL, f"G4 {err}"
+    assert og.rel_frobenius(y, r) < 5e-3
+
+
+@pytest.mark.parametrize("M", [16, 200])
+def test_gemm_transposed_output_and_gamma(fireq, M):
+    y, r, *_ = run_case(fireq, M, 256, 512, gamma=True, out_layout=1, seed=M)
+    assert og.g4_error(y, r) <= G4_TOL
+
+
+def test_gemm_exactness_corridor(fireq):
+    """Integer operands, sigma = 1, beta = 1, n = 0, |partial sums| <= 256: bit-exact."""
+    rng = np.random.default_rng(5)
+    M, N, K = 16, 256, 1024
+    codes = rng.integers(-2, 3, size=(N, K)).astype(np.int8)
+    sc = np.full((N, K // 128), 56, dtype=np.uint8)           # E4M3 code 56 = 1.0
+    sc[7, 3] = 0                                              # a zero-scale group contributes 0
+    xi = np.zeros((M, K))
+    for m in range(M):
+        idx = rng.choice(K, 64, replace=False)
+        xi[m, idx] = rng.integers(-2, 3, 64)
+    packed = torch.from_numpy(ol.pack_codes(codes)).to(DEV)
+    scales = torch.from_numpy(ol.pack_scales(sc)).to(DEV)
+    xq = torch.from_numpy(nm.e4m3_encode(xi)).to(DEV)
+    beta = torch.ones(M, dtype=torch.bfloat16, device=DEV)
+    Y = fireq.w4a8_gemm(xq, beta, packed, scales, N, 0)
+    wv = codes.astype(np.float64)
+    wv[7, 384:512] = 0
+    exact = xi @ wv.T
+    assert np.abs(exact).max() <= 256
+    assert np.array_equal(Y.float().cpu().numpy().astype(np.float64), exact)
+
+
+def test_gemm_deterministic(fireq):
+    M, N, K = 16, 1024, 4096
+    wb = synth.weights(N, K, 11)
+    xb = synth.activations(M, K, 12)
+    qw = fireq.quantize_weight(to_dev_bf16(wb))
+    xq, beta = fireq.quantize_act(to_dev_bf16(xb), chan_mul=qw.c)
+    ws = fireq.Workspace(fireq.gemm_workspace_bytes(M, N, K))
+    y1 = fireq.w4a8_gemm(xq, beta, qw.packed, qw.scales, N, qw.n, workspace=ws)
+    y2 = fireq.w4a8_gemm(xq, beta, qw.packed, qw.scales, N, qw.n, workspace=ws)
+    assert torch.equal(y1, y2)
+    assert int(ws.t[: 4 * (N // 128)].view(torch.int32).abs().sum()) == 0   # counters left zeroed
+
+
+@pytest.mark.parametrize("name,M", [("llama2-7b.gate", 16), ("llama2-7b.down", 16), ("llama3-8b.k", 16),
+                                    ("llama3-8b.down", 16), ("llama2-7b.up", 1024)])
+def test_gemm_full_size_sampled(fireq, name, M):
+    """BASELINE full shapes in the bench's launch configuration; oracle on sampled channels.
+
+    The oracle quantizes the whole tensor (CAS and PTS are global) and the fp64
+    reference is formed for 192 sampled output channels; the GPU packing of those
+    rows is also compared bit-exactly with the oracle's codes and scales.
+    """
+    N, K = synth.SHAPES[name]
+    wb = synth.weights(N, K, synth.layer_seed(1, 0))
+    xb = synth.activations(M, K, synth.layer_seed(1, 1))
+    qw = fireq.quantize_weight(to_dev_bf16(wb), cas_mode=1)
+    xq, beta = fireq.quantize_act(to_dev_bf16(xb), chan_mul=qw.c)
+    Y = fireq.w4a8_gemm(xq, beta, qw.packed, qw.scales, N, qw.n)
+    torch.cuda.synchronize()
+    ref = oq.quantize_weight(synth.bits_to_f64(wb), 1, pack=False)
+    assert qw.n == ref.n
+    rq, rbeta = oq.quantize_act(synth.bits_to_f64(xb), ref.c)
+    assert np.array_equal(xq.cpu().numpy(), rq)
+    rows = np.sort(np.random.default_rng(3).choice(N, 192, replace=False))
+    # GPU packing of the sampled rows == oracle codes / scale codes
+    packed = qw.packed.cpu().numpy()
+    scales = qw.scales.cpu().numpy()
+    kk = np.arange(K)
+    for n in rows[:16]:
+        byte, half = ol.packed_byte_index(np.full(K, n), kk, K)
+        nib = np.where(half == 0, packed[byte] & 15, packed[byte] >> 4).astype(np.int16)
+        assert np.array_equal(np.where(nib >= 8, nib - 16, nib), ref.codes[n])
+        assert np.array_equal(scales[ol.scale_index(np.full(K // 128, n), np.arange(K // 128), K)],
+                              ref.sigma_codes[n])
+    table = og.lut_of_luts()
+    wdeq = nm.E4M3_DECODE[table[np.repeat(ref.sigma_codes[rows].astype(np.int64), 128, axis=1),
+                                ref.codes[rows].astype(np.int64) & 15]]
+    r = og.reference_rows(rq, rbeta, wdeq, ref.n)
+    y = Y.float().cpu().numpy().astype(np.float64)[:, rows]
+    assert og.g4_error(y, r) <= G4_TOL
