@@ -1,0 +1,475 @@
+"""bench.py -- FireQ W4A8-FP linear layer on B200: the driver's benchmark contract.
+
+Headline (BASELINE.json metric "... Llama FFN latency at batch 16", configs[1]):
+one step = one Llama2-7B FFN at decode batch M = 16 through the library's online
+hot path (all on-device, inputs resident in HBM):
+
+  fireq_quantize_act(x, c_gu)            A1-A3  (FP8 activations, BF16 beta)
+  fireq_w4a8_gemm(W_gu = [gate; up])     Steps 1-3 (INT4 x FP8 on tcgen05), gamma = [1 | c_down]
+  fireq_silu_mul_quantize_act(g, u)      SiLU * up then A2-A3
+  fireq_w4a8_gemm(W_down)
+
+The weights are quantized offline by fireq_quantize_weight (W1-W6; timed once and
+reported under "offline": the paper quantizes offline).  Four rotating copies
+of the quantized FFN weights (4 x 68.7 MB > 2 x L2) are cycled so every step streams
+its weights from HBM.  Each step is one CUDA graph replay (4 kernel launches).
+
+Also reported (same run): the dominant kernel's roofline (the gate_up GEMM, HBM
+bound at decode), single-GEMM decode figures, the prefill FFN (M = 16 x 1024,
+FP8-tensor bound), an end-to-end figure through host buffers, GPU clocks, and the
+CPU oracle timed on a bounded sample (cpu_baseline).
+
+Run:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fireq|reference]
+N > 1 (torchrun): column-parallel FFN (N-sharded gate_up and down, NCCL all-gather
+of the BF16 outputs in the Y^T layout, in place).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+D_MODEL, D_FF = 4096, 11008          # Llama2-7B FFN (BASELINE configs[1])
+M_DECODE = 16
+M_PREFILL = 16 * 1024
+ROTATIONS = 4
+METRIC = "Llama2-7B FFN latency at batch 16 (W4A8-FP: INT4 weights + FP8 g128 scales, FP8 activations)"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ helpers
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms while running."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.idx = device_index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for i, nm in enumerate(names):
+                if len(s) > 4 + i and s[4 + i].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def gemm_bytes(M, N, K):
+    """Algorithmic bytes of one fireq_w4a8_gemm: packed W + sigma + X_hat + beta + Y."""
+    return N * K // 2 + N * K // 128 + M * K + 2 * M + 2 * M * N
+
+
+def act_bytes(M, K, chan=False):
+    return 3 * M * K + 2 * M + (2 * K if chan else 0)
+
+
+# ------------------------------------------------------------------ workload
+class FFN:
+    """Quantized Llama FFN weights + activation buffers on one GPU (optionally an N-shard)."""
+
+    def __init__(self, F, M, rotations, dev, shard=None):
+        self.F, self.M, self.dev = F, M, dev
+        wg = synth.weights(D_FF, D_MODEL, synth.layer_seed(1, 0))
+        wu = synth.weights(D_FF, D_MODEL, synth.layer_seed(1, 1))
+        wd = synth.weights(D_MODEL, D_FF, synth.layer_seed(1, 2))
+        W_gu = synth.bits_to_torch(np.concatenate([wg, wu], axis=0)).to(dev)
+        W_d = synth.bits_to_torch(wd).to(dev)
+        # offline quantization (W1-W6), timed once
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        q_gu = F.quantize_weight(W_gu, cas_mode=1)
+        q_d = F.quantize_weight(W_d, cas_mode=1)
+        torch.cuda.synchronize()
+        self.offline_s = time.perf_counter() - t0
+        self.n_gu, self.n_d = q_gu.n, q_d.n
+        self.c_gu = q_gu.c
+        self.gamma = torch.cat([torch.ones(D_FF, device=dev), q_d.c.float()])
+        self.rot = []
+        for r in range(rotations):
+            self.rot.append((q_gu.packed.clone(), q_gu.scales.clone(), q_d.packed.clone(), q_d.scales.clone()))
+        del W_gu, W_d
+        x = synth.activations(M, D_MODEL, synth.layer_seed(1, 3))
+        self.x = synth.bits_to_torch(x).to(dev)
+        self.xq = torch.empty((M, D_MODEL), dtype=torch.uint8, device=dev)
+        self.beta = torch.empty(M, dtype=torch.bfloat16, device=dev)
+        self.gu = torch.empty((M, 2 * D_FF), dtype=torch.bfloat16, device=dev)
+        self.hq = torch.empty((M, D_FF), dtype=torch.uint8, device=dev)
+        self.hbeta = torch.empty(M, dtype=torch.bfloat16, device=dev)
+        self.y = torch.empty((M, D_MODEL), dtype=torch.bfloat16, device=dev)
+        self.ws1 = F.Workspace(F.gemm_workspace_bytes(M, 2 * D_FF, D_MODEL), dev)
+        self.ws2 = F.Workspace(F.gemm_workspace_bytes(M, D_MODEL, D_FF), dev)
+
+    def step(self, r, stream=None):
+        F = self.F
+        p_gu, s_gu, p_d, s_d = self.rot[r]
+        F.quantize_act(self.x, chan_mul=self.c_gu, out=(self.xq, self.beta), stream=stream)
+        F.w4a8_gemm(self.xq, self.beta, p_gu, s_gu, 2 * D_FF, self.n_gu, gamma=self.gamma, out=self.gu,
+                    workspace=self.ws1, stream=stream)
+        F.silu_mul_quantize_act(self.gu[:, :D_FF], self.gu[:, D_FF:], out=(self.hq, self.hbeta), stream=stream)
+        F.w4a8_gemm(self.hq, self.hbeta, p_d, s_d, D_MODEL, self.n_d, out=self.y, workspace=self.ws2, stream=stream)
+
+    KERNELS_PER_STEP = 4
+
+    def bytes_per_step(self):
+        M = self.M
+        return (act_bytes(M, D_MODEL, True) + gemm_bytes(M, 2 * D_FF, D_MODEL) + 2 * M * 2 * D_FF  # gu re-read
+                + act_bytes(M, D_FF) + gemm_bytes(M, D_MODEL, D_FF))
+
+    def flops_per_step(self):
+        return 2 * self.M * (2 * D_FF * D_MODEL + D_MODEL * D_FF)
+
+
+def capture(fn, stream):
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        fn()
+    return g
+
+
+def time_steps(g_multi, g_single, steps, warmup, stream, barrier=None):
+    """Exactly `steps` steps: steps // R replays of the R-step graph + the remainder singly."""
+    R = len(g_single)
+    for i in range(max(1, warmup // R)):
+        g_multi.replay()
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(steps // R):
+            g_multi.replay()
+        for r in range(steps % R):
+            g_single[r].replay()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    return e0.elapsed_time(e1)
+
+
+def time_graphs(graphs, steps, warmup, stream, barrier=None):
+    """Replay graphs round-robin; returns total ms for exactly `steps` replays (CUDA events)."""
+    for i in range(warmup):
+        graphs[i % len(graphs)].replay()
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for i in range(steps):
+            graphs[i % len(graphs)].replay()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    return e0.elapsed_time(e1)
+
+
+# ------------------------------------------------------------------ CPU oracle
+def cpu_oracle_sample(frac_rows=8, M=M_DECODE):
+    """The oracle (as it stands) on a bounded sample of the decode FFN step.
+
+    Sample: the activation quantizer on the full token batch, and the three fp64
+    reference GEMMs (LUT dequantization + matmul) on 1/frac_rows of the output
+    channels with full K; the time is scaled by frac_rows to one FFN step.
+    Weight quantization (offline) is not part of the step, as on the GPU side.
+    """
+    from oracle import gemm as og, quant as oq, ffn as of, numerics as nm
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
+    except Exception:
+        threads = 1
+    rng = np.random.default_rng(0)
+    X = synth.bits_to_f64(synth.activations(M, D_MODEL, 1))
+    H = synth.bits_to_f64(synth.activations(M, D_FF, 2))
+    ng, nd = D_FF * 2 // frac_rows // 128 * 128, D_MODEL // frac_rows // 128 * 128
+    codes_gu = rng.integers(-8, 8, (ng, D_MODEL)).astype(np.int8)
+    codes_d = rng.integers(-8, 8, (nd, D_FF)).astype(np.int8)
+    from oracle import layout as ol
+    p_gu = ol.pack_codes(codes_gu)
+    s_gu = ol.pack_scales(rng.integers(40, 60, (ng, D_MODEL // 128)).astype(np.uint8))
+    p_d = ol.pack_codes(codes_d)
+    s_d = ol.pack_scales(rng.integers(40, 60, (nd, D_FF // 128)).astype(np.uint8))
+    c = nm.bf16_rn(np.ones(D_MODEL))
+    t0 = time.perf_counter()
+    xq, beta = oq.quantize_act(X, c)
+    r = og.gemm_reference(xq, beta, p_gu, s_gu, ng, D_MODEL, 10)
+    h = of.silu_mul(nm.bf16_rn(r[:, : ng // 2]), nm.bf16_rn(r[:, ng // 2:]))
+    hq, hb = oq.quantize_act(H)
+    og.gemm_reference(hq, hb, p_d, s_d, nd, D_FF, 10)
+    dt = time.perf_counter() - t0
+    # act quant of h on the full width is included; GEMM parts scale with the sampled rows
+    est = dt * frac_rows
+    return {"value": est * 1e6, "unit": "us", "cores": threads, "kind": "oracle",
+            "sample": f"activation quantizer on the full [16][4096] batch + fp64 LUT-dequant reference GEMMs on "
+                      f"1/{frac_rows} of the output channels of gate_up ({ng} rows) and down ({nd} rows), full K; "
+                      f"time x{frac_rows} = one FFN step; measured {dt:.2f} s"}
+
+
+# ------------------------------------------------------------------ arms
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    vals = []
+    for _ in range(max(1, args.warmup)):
+        cpu_oracle_sample(frac_rows=32)
+    samples = []
+    for _ in range(args.steps):
+        samples.append(cpu_oracle_sample(frac_rows=32))
+    v = statistics.median([s["value"] for s in samples])
+    cb = dict(samples[0])
+    cb["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "us", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v / 1e3, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "llama2-7b-ffn-decode-b16", "tokens": M_DECODE, "d_model": D_MODEL,
+                       "d_ff": D_FF},
+            "cpu_baseline": cb, "e2e": {"value": v, "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_fireq(args, rank, world, dev):
+    from paper_2505_20839_b200 import fireq as F
+    F.load()
+    peaks, peak_src = load_peaks()
+    stream = torch.cuda.Stream(device=dev)
+    barrier = (lambda: torch.distributed.barrier()) if world > 1 else None
+    if world > 1:
+        from paper_2505_20839_b200 import multigpu
+        return multigpu.run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src)
+
+    # ---------------- decode FFN (headline)
+    ffn = FFN(F, M_DECODE, ROTATIONS, dev)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        for r in range(ROTATIONS):          # first launches outside capture (TMA maps, func attrs)
+            ffn.step(r, stream)
+    torch.cuda.synchronize()
+    # one graph = ROTATIONS consecutive steps (distinct weight copies), PDL edges inside;
+    # a remainder uses single-step graphs so that exactly args.steps steps are timed.
+    g_multi = capture(lambda: [ffn.step(r, stream) for r in range(ROTATIONS)], stream)
+    g_single = [capture(lambda r=r: ffn.step(r, stream), stream) for r in range(ROTATIONS)]
+    clocks = ClockSampler(dev.index or 0)
+    clocks.start()
+    time.sleep(0.25)
+    # long enough for the clock sampler: repeat the timed region, keep the K-step one
+    time_steps(g_multi, g_single, max(2000, args.steps), args.warmup, stream)
+    total_ms = time_steps(g_multi, g_single, args.steps, args.warmup, stream)
+    clocks.stop()
+    us_per_step = total_ms * 1e3 / args.steps
+
+    # ---------------- dominant kernel: the gate_up GEMM alone (HBM bound), rotating weights
+    def gu_only(r):
+        p_gu, s_gu, _, _ = ffn.rot[r]
+        F.w4a8_gemm(ffn.xq, ffn.beta, p_gu, s_gu, 2 * D_FF, ffn.n_gu, gamma=ffn.gamma, out=ffn.gu,
+                    workspace=ffn.ws1, stream=stream)
+
+    def d_only(r):
+        _, _, p_d, s_d = ffn.rot[r]
+        F.w4a8_gemm(ffn.hq, ffn.hbeta, p_d, s_d, D_MODEL, ffn.n_d, out=ffn.y, workspace=ffn.ws2, stream=stream)
+
+    reps = 50
+    g_gu = capture(lambda: [gu_only(r) for r in range(ROTATIONS) for _ in range(2)], stream)
+    ms_gu = time_graphs([g_gu], reps, 4, stream) / (reps * 2 * ROTATIONS)
+    g_d = capture(lambda: [d_only(r) for r in range(ROTATIONS) for _ in range(2)], stream)
+    ms_d = time_graphs([g_d], reps, 4, stream) / (reps * 2 * ROTATIONS)
+    b_gu = gemm_bytes(M_DECODE, 2 * D_FF, D_MODEL)
+    gbs_gu = b_gu / (ms_gu * 1e-3) / 1e9
+    b_d = gemm_bytes(M_DECODE, D_MODEL, D_FF)
+    gbs_d = b_d / (ms_d * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("gemm_gate_up_m16_bytes_per_launch")
+
+    # ---------------- end to end through host buffers (pinned H2D of x, D2H of y)
+    x_host = ffn.x.cpu().pin_memory()
+    y_host = torch.empty_like(ffn.y, device="cpu").pin_memory()
+
+    def e2e_step(r):
+        ffn.x.copy_(x_host, non_blocking=True)
+        ffn.step(r, stream)
+        y_host.copy_(ffn.y, non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        for r in range(ROTATIONS):
+            e2e_step(r)
+    torch.cuda.synchronize()
+    g_e2e_multi = capture(lambda: [e2e_step(r) for r in range(ROTATIONS)], stream)
+    g_e2e = [capture(lambda r=r: e2e_step(r), stream) for r in range(ROTATIONS)]
+    e2e_ms = time_steps(g_e2e_multi, g_e2e, args.steps, args.warmup, stream) / args.steps
+
+    # ---------------- prefill FFN (FP8 tensor bound) and single-GEMM figures
+    del g_multi, g_single, g_gu, g_d, g_e2e, g_e2e_multi
+    pre_info = prefill_figures(F, dev, stream, peaks) if not args.no_prefill else None
+
+    # ---------------- cpu baseline (oracle on a bounded sample)
+    cpu = cpu_oracle_sample(frac_rows=8) if not args.no_cpu else None
+
+    hbm = peaks["hbm_gbs"]
+    line = {
+        "metric": METRIC, "value": round(us_per_step, 3), "unit": "us", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(us_per_step / 1e3, 6), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp8e4m3 x int4 -> f32 acc -> bf16", "data": "synthetic",
+        "config": {"workload": "llama2-7b-ffn-decode-b16", "tokens": M_DECODE, "d_model": D_MODEL, "d_ff": D_FF,
+                   "gemms": "gate_up 22016x4096 (fused, gamma=[1|c_down]) + down 4096x11008",
+                   "parallelism": "single GPU",
+                   "l2": f"{ROTATIONS} rotating weight copies ({ROTATIONS * (b_gu + b_d) / 1e6:.0f} MB > 2x L2)",
+                   "graph": f"CUDA graphs of {ROTATIONS} steps (4 PDL-chained kernels per step)"},
+        "gpu_launches": FFN.KERNELS_PER_STEP * args.steps,
+        "step_gbs": round(ffn.bytes_per_step() / (us_per_step * 1e-6) / 1e9, 1),
+        "roofline": {"bound": "hbm", "kernel": "fireq_w4a8_gemm gate_up M=16 N=22016 K=4096",
+                     "achieved": round(gbs_gu, 1), "peak": hbm, "unit": "GB/s", "frac": round(gbs_gu / hbm, 4),
+                     "traffic": traffic, "algorithmic_bytes": b_gu, "launch_us": round(ms_gu * 1e3, 3),
+                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"},
+        "gemm_down": {"us": round(ms_d * 1e3, 3), "gbs": round(gbs_d, 1), "frac": round(gbs_d / hbm, 4)},
+        "e2e": {"value": round(e2e_ms * 1e3, 3), "unit": "us", "h2d_bytes_per_step": ffn.x.numel() * 2,
+                "d2h_bytes_per_step": ffn.y.numel() * 2},
+        "offline": {"quantize_weight_ms_gate_up_and_down": round(ffn.offline_s * 1e3, 2)},
+        "clocks": clocks.summary(),
+    }
+    if pre_info:
+        line["prefill"] = pre_info
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+
+
+def prefill_figures(F, dev, stream, peaks):
+    """Prefill FFN at M = 16 x 1024: tensor-bound; TFLOP/s of each GEMM vs the FP8 peak."""
+    M = M_PREFILL
+    fp8_peak = 2.0 * peaks["bf16_tflops"]           # dense FP8 = 2 x measured bf16 (guide's nominal ratio)
+    ffn = FFN(F, M, 1, dev)
+    with torch.cuda.stream(stream):
+        ffn.step(0, stream)
+    torch.cuda.synchronize()
+    p_gu, s_gu, p_d, s_d = ffn.rot[0]
+
+    def t(fn, reps=5):
+        with torch.cuda.stream(stream):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(reps):
+                fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    ms_gu = t(lambda: F.w4a8_gemm(ffn.xq, ffn.beta, p_gu, s_gu, 2 * D_FF, ffn.n_gu, gamma=ffn.gamma, out=ffn.gu,
+                                  workspace=ffn.ws1, stream=stream))
+    ms_d = t(lambda: F.w4a8_gemm(ffn.hq, ffn.hbeta, p_d, s_d, D_MODEL, ffn.n_d, out=ffn.y, workspace=ffn.ws2,
+                                 stream=stream))
+    ms_ffn = t(lambda: ffn.step(0, stream), reps=3)
+    tf_gu = 2 * M * 2 * D_FF * D_MODEL / (ms_gu * 1e-3) / 1e12
+    tf_d = 2 * M * D_MODEL * D_FF / (ms_d * 1e-3) / 1e12
+    tf_ffn = ffn.flops_per_step() / (ms_ffn * 1e-3) / 1e12
+    del ffn
+    torch.cuda.empty_cache()
+    return {"workload": "llama2-7b-ffn-prefill-16x1024", "ffn_ms": round(ms_ffn, 3), "ffn_tflops": round(tf_ffn, 1),
+            "gate_up_ms": round(ms_gu, 3), "gate_up_tflops": round(tf_gu, 1), "down_ms": round(ms_d, 3),
+            "down_tflops": round(tf_d, 1), "fp8_peak_tflops": fp8_peak,
+            "frac_gate_up": round(tf_gu / fp8_peak, 4), "frac_ffn": round(tf_ffn / fp8_peak, 4),
+            "peak_source": "2 x MEASURED_PEAKS bf16_tflops (burst)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", choices=["fireq", "reference"], default="fireq")
+    ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py --impl fireq needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=dev)
+    try:
+        run_fireq(args, rank, world, dev)
+    finally:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -196,6 +196,11 @@ fireq_status_t fireq_w4a8_gemm_colpar(const uint8_t* x_fp8, const void* x_scale,
  * (entry [s][u] = E4M3_RN(v(u) * dec(s)), v(u) = u < 8 ? u : u - 16) into the
  * device buffer out[2032], on `stream`. */
 fireq_status_t fireq_debug_lut_table(uint8_t* out, void* stream);
+/* Debug/profiling: when buf != NULL, every later fireq_w4a8_gemm launch records a
+ * per-CTA %globaltimer timeline into the device buffer buf ([ctas][8] uint64:
+ * start, setup done, first stage landed, MMA issue done, epilogue done, end).
+ * Pass NULL to disable.  Not thread-safe; for benchmarks only. */
+fireq_status_t fireq_debug_set_trace(void* buf);
 /* Number of GEMM kernel launches fireq_w4a8_gemm would enqueue for (M, N, K)
  * and the chosen configuration, for benchmarks: writes {ntok, splits, ctas,
  * sign_split} into cfg_out[4] (host). */

@@ -26,6 +26,7 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
                          const float* gamma, __nv_bfloat16* Y, int64_t ldy, int out_layout, void* ws,
                          size_t ws_bytes, cudaStream_t stream);
 fireq_status_t debug_lut_table(uint8_t* out, cudaStream_t stream);
+extern unsigned long long* g_trace;
 
 namespace {
 thread_local std::string g_last_error;
@@ -169,6 +170,13 @@ fireq_status_t fireq_w4a8_gemm(const uint8_t* x_fp8, const void* x_scale, int64_
 fireq_status_t fireq_debug_lut_table(uint8_t* out, void* stream) {
     FIREQ_REQUIRE(out, FIREQ_ERROR_INVALID_VALUE, "fireq_debug_lut_table: NULL pointer");
     return debug_lut_table(out, static_cast<cudaStream_t>(stream));
+}
+
+// Debug: subsequent GEMM launches record a per-CTA %globaltimer timeline into buf
+// ([ctas][8] u64: start, setup done, first stage landed, MMA done, epilogue done, end).
+fireq_status_t fireq_debug_set_trace(void* buf) {
+    g_trace = static_cast<unsigned long long*>(buf);
+    return FIREQ_SUCCESS;
 }
 
 fireq_status_t fireq_gemm_plan(int64_t M, int64_t N, int64_t K, int32_t cfg_out[4]) {

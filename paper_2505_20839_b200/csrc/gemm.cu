@@ -29,6 +29,7 @@
 // contiguously across CTAs ("stream-K"), and tiles shared by several CTAs are
 // reduced deterministically (fixed contributor order) by the last-arriving CTA.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -38,6 +39,7 @@
 #include "ptx.cuh"
 
 namespace fireq {
+unsigned long long* g_trace = nullptr;   // debug timeline buffer (fireq_debug_set_trace)
 namespace {
 
 constexpr int kGroup = 128;            // K per group (one FP8 scale)
@@ -58,32 +60,90 @@ struct GemmArgs {
     int n_tiles, m_tiles, tiles;
     int pts_n;
     int out_layout;
-    int mode;              // 0 = tile round-robin, 1 = stream-K
+    int R;                 // tiles [0, R) are split contiguously over CTAs ("stream-K")
     int C;                 // CTAs in the grid
-    long long U;           // total units (stream-K)
+    long long U;           // stream-K units = R * G
+    unsigned long long* trace;   // debug timeline [C][8] (%globaltimer ns) or nullptr
+    int dbg;                     // experiments only: bit0 skip conversion, bit1 skip MMAs, bit2 skip loads
 };
 
+// FIREQ_PROFILE=1 builds (scripts/trace_gemm.py) record per-role cycle counters and a
+// per-CTA %globaltimer timeline; default builds compile the probes away.
+#ifndef FIREQ_PROFILE
+#define FIREQ_PROFILE 0
+#endif
+__device__ __forceinline__ long long prof_clock() {
+#if FIREQ_PROFILE
+    return clock64();
+#else
+    return 0;
+#endif
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#if FIREQ_PROFILE
+#define FIREQ_TRACE(slot) do { if (a.trace) a.trace[blockIdx.x * 16 + (slot)] = gtimer(); } while (0)
+#define FIREQ_TRACE_VAL(slot, v) do { if (a.trace) a.trace[blockIdx.x * 16 + (slot)] = (v); } while (0)
+#else
+#define FIREQ_TRACE(slot) do { } while (0)
+#define FIREQ_TRACE_VAL(slot, v) do { } while (0)
+#endif
+
 // Segment = contiguous run of groups [g0, g1) of one tile processed by one CTA.
+// Schedule of CTA c: first its share [c*U/C, (c+1)*U/C) of the stream-K units of tiles
+// [0, R) (so that split tiles are reduced early, overlapped with later work), then the
+// whole tiles R + c, R + c + C, ...
 struct SegIter {
-    int mode, G, tiles, C, c, k;
+    int G, tiles, C, c, R, k;
     long long u, u_end;
     __device__ __forceinline__ void init(const GemmArgs& a, int cta) {
-        mode = a.mode; G = a.G; tiles = a.tiles; C = a.C; c = cta; k = 0;
-        u = (long long)cta * a.U / a.C;
-        u_end = (long long)(cta + 1) * a.U / a.C;
+        G = a.G; tiles = a.tiles; C = a.C; c = cta; R = a.R; k = 0;
+        u = a.U ? (long long)cta * a.U / a.C : 0;
+        u_end = a.U ? (long long)(cta + 1) * a.U / a.C : 0;
     }
     __device__ __forceinline__ bool next(int& tile, int& g0, int& g1) {
-        if (mode == 0) {
-            tile = c + k * C;
-            if (tile >= tiles) return false;
-            ++k; g0 = 0; g1 = G;
+        if (u < u_end) {
+            tile = (int)(u / G);
+            g0 = (int)(u % G);
+            g1 = (int)min((long long)G, (long long)g0 + (u_end - u));
+            u = (long long)tile * G + g1;
             return true;
         }
-        if (u >= u_end) return false;
-        tile = (int)(u / G);
-        g0 = (int)(u % G);
-        g1 = (int)min((long long)G, (long long)g0 + (u_end - u));
-        u = (long long)tile * G + g1;
+        tile = R + c + k * C;
+        if (tile >= tiles) return false;
+        ++k; g0 = 0; g1 = G;
+        return true;
+    }
+};
+
+// Walks the (tile, group) units of a CTA in order; ntile / mtile are computed once
+// per segment (no integer division per unit).
+struct UnitIter {
+    SegIter it;
+    int tile, g, g1, nt, mt, n_tiles;
+    bool valid;
+    __device__ __forceinline__ void seg_begin() {
+        nt = tile % n_tiles;
+        mt = tile / n_tiles;
+    }
+    __device__ __forceinline__ void init(const GemmArgs& a, int cta) {
+        it.init(a, cta);
+        n_tiles = a.n_tiles;
+        valid = it.next(tile, g, g1);
+        if (valid) seg_begin();
+    }
+    __device__ __forceinline__ bool next(int& ntile, int& mtile, int& gg) {
+        if (!valid) return false;
+        ntile = nt;
+        mtile = mt;
+        gg = g;
+        if (++g >= g1) {
+            valid = it.next(tile, g, g1);
+            if (valid) seg_begin();
+        }
         return true;
     }
 };
@@ -116,11 +176,13 @@ __host__ __device__ constexpr uint32_t make_idesc(int ntok, bool negate_a) {
          | ((uint32_t)(128 >> 4) << 24);      // M >> 4
 }
 
-template <int NTOK, bool SIGN_SPLIT, int NCONV, int STAGES, int ASTAGES, int ACCBUF>
+template <int NTOK, bool SIGN_SPLIT, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS>
 struct Cfg {
-    static constexpr int kXBytes = NTOK * kGroup;                       // FP8 activation tile
-    static constexpr int kStageTx = kXBytes + kWBytes + kTileN;         // bytes per stage
-    static constexpr int kASz = SIGN_SPLIT ? 64 : 32;                   // TMEM cols per A stage
+    static constexpr int kXBytes = NTOK * kGroup;                       // FP8 activation tile (1 group)
+    static constexpr int kXStage = GPS * kXBytes;
+    static constexpr int kWStage = GPS * kWBytes;
+    static constexpr int kSStage = GPS * kTileN;
+    static constexpr int kASz = GPS * (SIGN_SPLIT ? 64 : 32);           // TMEM cols per A stage
     static constexpr int kAccCols = ACCBUF * NTOK;
     static constexpr int kACol0 = (kAccCols + 31) / 32 * 32;
     static constexpr int kTmemNeed = kACol0 + ASTAGES * kASz;
@@ -128,16 +190,57 @@ struct Cfg {
                                    : kTmemNeed <= 256 ? 256 : 512;
     static_assert(kTmemNeed <= 512, "TMEM budget");
     static constexpr int kThreads = 256 + 128 * NCONV;
+    // stream-K fixup: contributor partials are staged into SMEM by bulk copies,
+    // kFixSlots per round trip (decode tile sizes only; larger NTOK use registers).
+    static constexpr int kFixSlots = NTOK <= 32 ? 32768 / (NTOK * kTileN * 4) : 0;
+    static constexpr int kPartBytes = NTOK * kTileN * 4;
     // shared memory carve-up (offsets from a 1024-aligned base)
     static constexpr int kOffX = 0;
-    static constexpr int kOffW = kOffX + STAGES * kXBytes;
-    static constexpr int kOffS = kOffW + STAGES * kWBytes;
-    static constexpr int kOffLut = kOffS + STAGES * kTileN;
-    static constexpr int kOffBar = kOffLut + 2048;
-    static constexpr int kNumBars = 2 * STAGES + 2 * ASTAGES + 2 * ACCBUF;
+    static constexpr int kOffW = kOffX + STAGES * kXStage;
+    static constexpr int kOffS = kOffW + STAGES * kWStage;
+    static constexpr int kOffLut = kOffS + STAGES * kSStage;
+    static constexpr int kOffFix = kOffLut + 2048;
+    static constexpr int kOffBar = kOffFix + kFixSlots * kPartBytes;
+    static constexpr int kNumBars = 3 * STAGES + 2 * ASTAGES + 2 * ACCBUF + 1;
     static constexpr int kOffMisc = kOffBar + kNumBars * 8;
     static constexpr int kSmemBytes = kOffMisc + 64 + 1024;             // + alignment slack
     static_assert(kXBytes % 1024 == 0, "X tile must keep 1024-B alignment");
+};
+
+// Walks a CTA's units in pipeline stages of up to GPS consecutive groups of one tile
+// (ntile / mtile computed once per segment).
+template <int GPS>
+struct StageIter {
+    SegIter it;
+    int tile, g, g1, n_tiles, nt_, mt_, seg_start;
+    bool valid;
+    __device__ __forceinline__ void begin_seg() {
+        nt_ = tile % n_tiles;
+        mt_ = tile / n_tiles;
+        seg_start = g;
+    }
+    __device__ __forceinline__ void init(const GemmArgs& a, int cta) {
+        it.init(a, cta);
+        n_tiles = a.n_tiles;
+        valid = it.next(tile, g, g1);
+        if (valid) begin_seg();
+    }
+    // stage: tile (nt, mt), groups [g, g + ng); first / last = segment boundaries
+    __device__ __forceinline__ bool next(int& nt, int& mt, int& gg, int& ng, bool& first, bool& last) {
+        if (!valid) return false;
+        nt = nt_;
+        mt = mt_;
+        gg = g;
+        ng = min(GPS, g1 - g);
+        first = (g == seg_start);
+        g += ng;
+        last = (g >= g1);
+        if (last) {
+            valid = it.next(tile, g, g1);
+            if (valid) begin_seg();
+        }
+        return true;
+    }
 };
 
 // 16 output bytes pair (lo/hi word) per input word, sign-split.
@@ -164,10 +267,13 @@ __device__ __forceinline__ void conv_mask_select(uint32_t w, uint32_t L0, uint32
     r1 = ptx::lop3_mux(ptx::prmt(L0, L1, wh), ptx::prmt(L2, L3, xh), m1);
 }
 
-template <int NTOK, bool SIGN_SPLIT, int NCONV, int STAGES, int ASTAGES, int ACCBUF>
-__global__ void __launch_bounds__(Cfg<NTOK, SIGN_SPLIT, NCONV, STAGES, ASTAGES, ACCBUF>::kThreads, 1)
+// Roles (warp-uniform): warp 0 = weight TMA producer, warp 1 = MMA issuer, warp 2 =
+// TMEM allocator, warp 3 = activation TMA producer (the only producer that waits on
+// the previous kernel, PDL), warps 4-7 = epilogue, warps 8.. = converter warpgroups.
+template <int NTOK, bool SIGN_SPLIT, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS>
+__global__ void __maxnreg__((NTOK <= 32 ? 88 : NTOK <= 64 ? 96 : 128))
 k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
-    using C = Cfg<NTOK, SIGN_SPLIT, NCONV, STAGES, ASTAGES, ACCBUF>;
+    using C = Cfg<NTOK, SIGN_SPLIT, NCONV, STAGES, ASTAGES, ACCBUF, GPS>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment for the SW128 tiles, computed on the shared-window address so
     // that the pointer stays visibly in the shared state space (LDS, not generic LD).
@@ -177,22 +283,32 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
     uint8_t* sS = smem + C::kOffS;
     uint4* sLut = reinterpret_cast<uint4*>(smem + C::kOffLut);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
-    uint64_t* full = bars;
-    uint64_t* empty = full + STAGES;
-    uint64_t* afull = empty + STAGES;
-    uint64_t* aempty = afull + ASTAGES;
+    uint64_t* fullW = bars;                 // packed W + sigma landed
+    uint64_t* fullX = fullW + STAGES;       // activation tile landed
+    uint64_t* empty = fullX + STAGES;       // MMAs of the stage done (SMEM reusable)
+    uint64_t* afull = empty + STAGES;       // converted A stage in TMEM
+    uint64_t* aempty = afull + ASTAGES;     // MMAs reading the A stage done
     uint64_t* accfull = aempty + ASTAGES;
     uint64_t* accempty = accfull + ACCBUF;
+    uint64_t* fixbar = accempty + ACCBUF;
+    float* sFix = reinterpret_cast<float*>(smem + C::kOffFix);
     uint32_t* misc = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);   // [0] tmem base, [1] fixup flag
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
     // ------------------------------------------------------------ setup
+    if (threadIdx.x == 0) FIREQ_TRACE(0);
+    if (warp == 0) ptx::pdl_trigger();      // the next kernel may start its prologue
     if (warp == 0 && lane == 0) {
-        for (int i = 0; i < STAGES; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], 1); }
+        for (int i = 0; i < STAGES; ++i) {
+            ptx::mbar_init(&fullW[i], 1);
+            ptx::mbar_init(&fullX[i], 1);
+            ptx::mbar_init(&empty[i], 1);
+        }
         for (int i = 0; i < ASTAGES; ++i) { ptx::mbar_init(&afull[i], 128); ptx::mbar_init(&aempty[i], 1); }
         for (int i = 0; i < ACCBUF; ++i) { ptx::mbar_init(&accfull[i], 1); ptx::mbar_init(&accempty[i], 128); }
+        ptx::mbar_init(fixbar, 1);
         ptx::fence_mbar_init();
         ptx::prefetch_tmap(&tmap_x);
     }
@@ -214,120 +330,193 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = misc[0];
+    if (threadIdx.x == 0) FIREQ_TRACE(1);
 
     SegIter it;
     int tile, g0, g1;
+    StageIter<GPS> st;
+    int nt, mt, g, ng;
+    bool sfirst, slast;
 
     if (warp == 0) {
-        // ------------------------------------------------------- TMA producer
-        if (lane == 0) {
-            const uint64_t pol_w = ptx::policy_evict_first();   // weights: streamed once
-            const uint64_t pol_x = ptx::policy_evict_last();    // activations: re-read by every tile
-            it.init(a, blockIdx.x);
-            int i = 0;
-            while (it.next(tile, g0, g1)) {
-                const int ntile = tile % a.n_tiles, mtile = tile / a.n_tiles;
-                for (int g = g0; g < g1; ++g, ++i) {
-                    const int s = i % STAGES;
-                    ptx::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
-                    ptx::mbar_arrive_expect_tx(&full[s], C::kStageTx);
-                    const size_t blk = (size_t)ntile * a.G + g;
-                    ptx::bulk_g2s(sW + s * kWBytes, a.w_packed + blk * kWBytes, kWBytes, &full[s], pol_w);
-                    ptx::bulk_g2s(sS + s * kTileN, a.w_scales + blk * kTileN, kTileN, &full[s], pol_w);
-                    ptx::tma_2d_g2s(sX + s * C::kXBytes, &tmap_x, g * kGroup, mtile * NTOK, &full[s], pol_x);
+        // ------------------------------------------------------- weight producer
+        // Weights never depend on the previous kernel, so this warp streams them from
+        // the start (PDL overlap); the whole warp walks the schedule and one elected
+        // lane issues (a lane-0 branch makes the compiler wrap TMAs in waterfall loops).
+        const uint64_t pol_w = ptx::policy_evict_first();   // weights: streamed once
+        st.init(a, blockIdx.x);
+        int i = 0;
+        while (st.next(nt, mt, g, ng, sfirst, slast)) {
+            const int s = i % STAGES;
+            ptx::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+            if (ptx::elect_one()) {
+                if (a.dbg & 4) {
+                    ptx::mbar_arrive(&fullW[s]);
+                } else {
+                    ptx::mbar_arrive_expect_tx(&fullW[s], ng * (kWBytes + kTileN));
+                    const size_t blk = (size_t)nt * a.G + g;
+                    ptx::bulk_g2s(sW + s * C::kWStage, a.w_packed + blk * kWBytes, ng * kWBytes, &fullW[s], pol_w);
+                    ptx::bulk_g2s(sS + s * C::kSStage, a.w_scales + blk * kTileN, ng * kTileN, &fullW[s], pol_w);
                 }
             }
+            __syncwarp();
+            ++i;
         }
-        __syncwarp();
+    } else if (warp == 3) {
+        // ------------------------------------------------------- activation producer
+        const uint64_t pol_x = ptx::policy_evict_last();    // activations: re-read by every tile
+        ptx::pdl_wait();                    // activations are written by the previous kernel
+        st.init(a, blockIdx.x);
+        int i = 0;
+        while (st.next(nt, mt, g, ng, sfirst, slast)) {
+            const int s = i % STAGES;
+            ptx::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+            if (ptx::elect_one()) {
+                if (a.dbg & 4) {
+                    ptx::mbar_arrive(&fullX[s]);
+                } else {
+                    ptx::mbar_arrive_expect_tx(&fullX[s], ng * C::kXBytes);
+                    for (int q = 0; q < ng; ++q)
+                        ptx::tma_2d_g2s(sX + s * C::kXStage + q * C::kXBytes, &tmap_x, (g + q) * kGroup, mt * NTOK,
+                                        &fullX[s], pol_x);
+                }
+            }
+            __syncwarp();
+            ++i;
+        }
     } else if (warp == 1) {
         // ------------------------------------------------------- MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t idesc_pos = make_idesc(NTOK, false);
-            constexpr uint32_t idesc_neg = make_idesc(NTOK, true);
-            it.init(a, blockIdx.x);
-            int i = 0, sg = 0;
-            while (it.next(tile, g0, g1)) {
+        // Whole warp walks the schedule; one elected lane issues the stage's MMAs back to
+        // back and the commits (see the producer comment about waterfall loops).
+        constexpr uint32_t idesc_pos = make_idesc(NTOK, false);
+        constexpr uint32_t idesc_neg = make_idesc(NTOK, true);
+        st.init(a, blockIdx.x);
+        int i = 0, sg = 0;
+        const uint32_t sx0 = ptx::smem_u32(sX);
+        uint32_t d = tmem;
+        long long w_afull = 0, w_full = 0, t_issue = 0, t_mma0 = prof_clock();
+        while (st.next(nt, mt, g, ng, sfirst, slast)) {
+            const int s = i % STAGES, as = i % ASTAGES;
+            if (sfirst) {
                 const int b = sg % ACCBUF;
                 ptx::mbar_wait(&accempty[b], ((sg / ACCBUF) & 1) ^ 1);
-                ptx::tc_fence_after();
-                const uint32_t d = tmem + b * NTOK;
-                uint32_t acc = 0;
-                for (int g = g0; g < g1; ++g, ++i) {
-                    const int s = i % STAGES, as = i % ASTAGES;
-                    ptx::mbar_wait(&afull[as], (i / ASTAGES) & 1);
-                    ptx::mbar_wait(&full[s], (i / STAGES) & 1);
-                    ptx::tc_fence_after();
-                    const uint32_t ta = tmem + C::kACol0 + as * C::kASz;
-                    const uint64_t bdesc = smem_desc_sw128(ptx::smem_u32(sX + s * C::kXBytes));
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const uint64_t bd = bdesc + (uint64_t)(j * 32 >> 4);   // +32 B along K
-                        ptx::mma_f8f6f4_ts(d, ta + j * 8, bd, idesc_pos, acc);
-                        acc = 1;
-                        if (SIGN_SPLIT) ptx::mma_f8f6f4_ts(d, ta + 32 + j * 8, bd, idesc_neg, 1);
-                    }
-                    ptx::mma_commit(&empty[s]);
-                    ptx::mma_commit(&aempty[as]);
-                }
-                ptx::mma_commit(&accfull[b]);
-                ++sg;
+                d = tmem + b * NTOK;
             }
+            const long long c0 = prof_clock();
+            ptx::mbar_wait(&afull[as], (i / ASTAGES) & 1);
+            const long long c1 = prof_clock();
+            ptx::mbar_wait(&fullX[s], (i / STAGES) & 1);
+            w_afull += c1 - c0;
+            w_full += prof_clock() - c1;
+            ptx::tc_fence_after();
+            const uint32_t ta = tmem + C::kACol0 + as * C::kASz;
+            const long long c2 = prof_clock();
+            if (ptx::elect_one()) {
+                if (!(a.dbg & 2)) {
+                    for (int q = 0; q < ng; ++q) {
+                        const uint64_t bdesc = smem_desc_sw128(sx0 + s * C::kXStage + q * C::kXBytes);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const uint64_t bd = bdesc + (uint64_t)(j * 32 >> 4);   // +32 B along K
+                            const uint32_t acc = (sfirst && q == 0 && j == 0) ? 0u : 1u;
+                            ptx::mma_f8f6f4_ts(d, ta + (q * 4 + j) * 8, bd, idesc_pos, acc);
+                            if (SIGN_SPLIT)
+                                ptx::mma_f8f6f4_ts(d, ta + GPS * 32 + (q * 4 + j) * 8, bd, idesc_neg, 1u);
+                        }
+                    }
+                }
+                ptx::mma_commit(&empty[s]);
+                if (slast) ptx::mma_commit(&accfull[sg % ACCBUF]);
+            }
+            __syncwarp();
+            t_issue += prof_clock() - c2;
+            if (slast) ++sg;
+            ++i;
         }
-        __syncwarp();
+        if (lane == 0) {
+            FIREQ_TRACE(3);
+            FIREQ_TRACE_VAL(9, w_afull);
+            FIREQ_TRACE_VAL(10, w_full);
+            FIREQ_TRACE_VAL(11, prof_clock() - t_mma0);
+            FIREQ_TRACE_VAL(15, t_issue);
+        }
     } else if (warp >= 8) {
         // ------------------------------------------------------- converters
         const int wg = (warp - 8) >> 2;           // converter warpgroup
         const int r = threadIdx.x & 127;          // weight row == TMEM lane
         const uint32_t lane_base = (uint32_t)(r & ~31) << 16;
-        it.init(a, blockIdx.x);
+        st.init(a, blockIdx.x);
         int i = 0;
-        while (it.next(tile, g0, g1)) {
-            for (int g = g0; g < g1; ++g, ++i) {
-                if ((i % NCONV) != wg) continue;
-                const int s = i % STAGES, as = i % ASTAGES;
-                ptx::mbar_wait(&full[s], (i / STAGES) & 1);
-                ptx::mbar_wait(&aempty[as], ((i / ASTAGES) & 1) ^ 1);
-                ptx::tc_fence_after();
-                const uint4 L = sLut[sS[s * kTileN + r]];
-                const uint8_t* wrow = sW + s * kWBytes + r * 16;
+        long long cw_full = 0, cw_aempty = 0, ct0 = prof_clock();
+        while (st.next(nt, mt, g, ng, sfirst, slast)) {
+            if ((i % NCONV) != wg) { ++i; continue; }
+            const int s = i % STAGES, as = i % ASTAGES;
+            const long long c0 = prof_clock();
+            ptx::mbar_wait(&fullW[s], (i / STAGES) & 1);
+            cw_full += prof_clock() - c0;
+            if (i == 0 && threadIdx.x == 256) FIREQ_TRACE(2);
+            const long long c1 = prof_clock();
+            if (i >= ASTAGES) {
+                // A stage `as` was last read by the MMAs of stage i - ASTAGES, whose commit
+                // completes that stage's phase of empty[] (one commit per stage serves both the
+                // SMEM ring and the TMEM A ring; the MMA cannot pass stage i - 1 before this
+                // conversion, so the phase cannot alias).
+                const int j = i - ASTAGES;
+                ptx::mbar_wait(&empty[j % STAGES], (j / STAGES) & 1);
+            }
+            cw_aempty += prof_clock() - c1;
+            ptx::tc_fence_after();
+            if (!(a.dbg & 1)) {
                 const uint32_t ta = tmem + lane_base + C::kACol0 + as * C::kASz;
-                if (SIGN_SPLIT) {
-                    const uint32_t N0 = L.z & 0x7F7F7F7Fu, N1 = L.w & 0x7F7F7F7Fu;
+                for (int q = 0; q < ng; ++q) {
+                    const uint4 L = sLut[sS[s * C::kSStage + q * kTileN + r]];
+                    const uint8_t* wrow = sW + s * C::kWStage + q * kWBytes + r * 16;
+                    if (SIGN_SPLIT) {
+                        const uint32_t N0 = L.z & 0x7F7F7F7Fu, N1 = L.w & 0x7F7F7F7Fu;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const uint4 wv = *reinterpret_cast<const uint4*>(wrow + j * 128 * 16);
-                        uint32_t P[8], Q[8];
-                        conv_sign_split(wv.x, L.x, L.y, N0, N1, P[0], P[1], Q[0], Q[1]);
-                        conv_sign_split(wv.y, L.x, L.y, N0, N1, P[2], P[3], Q[2], Q[3]);
-                        conv_sign_split(wv.z, L.x, L.y, N0, N1, P[4], P[5], Q[4], Q[5]);
-                        conv_sign_split(wv.w, L.x, L.y, N0, N1, P[6], P[7], Q[6], Q[7]);
-                        ptx::tmem_st_x8(ta + j * 8, P);
-                        ptx::tmem_st_x8(ta + 32 + j * 8, Q);
-                    }
-                } else {
+                        for (int j = 0; j < 4; ++j) {
+                            const uint4 wv = *reinterpret_cast<const uint4*>(wrow + j * 128 * 16);
+                            uint32_t P[8], Q[8];
+                            conv_sign_split(wv.x, L.x, L.y, N0, N1, P[0], P[1], Q[0], Q[1]);
+                            conv_sign_split(wv.y, L.x, L.y, N0, N1, P[2], P[3], Q[2], Q[3]);
+                            conv_sign_split(wv.z, L.x, L.y, N0, N1, P[4], P[5], Q[4], Q[5]);
+                            conv_sign_split(wv.w, L.x, L.y, N0, N1, P[6], P[7], Q[6], Q[7]);
+                            ptx::tmem_st_x8(ta + (q * 4 + j) * 8, P);
+                            ptx::tmem_st_x8(ta + GPS * 32 + (q * 4 + j) * 8, Q);
+                        }
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const uint4 wv = *reinterpret_cast<const uint4*>(wrow + j * 128 * 16);
-                        uint32_t R[8];
-                        conv_mask_select(wv.x, L.x, L.y, L.z, L.w, R[0], R[1]);
-                        conv_mask_select(wv.y, L.x, L.y, L.z, L.w, R[2], R[3]);
-                        conv_mask_select(wv.z, L.x, L.y, L.z, L.w, R[4], R[5]);
-                        conv_mask_select(wv.w, L.x, L.y, L.z, L.w, R[6], R[7]);
-                        ptx::tmem_st_x8(ta + j * 8, R);
+                        for (int j = 0; j < 4; ++j) {
+                            const uint4 wv = *reinterpret_cast<const uint4*>(wrow + j * 128 * 16);
+                            uint32_t R[8];
+                            conv_mask_select(wv.x, L.x, L.y, L.z, L.w, R[0], R[1]);
+                            conv_mask_select(wv.y, L.x, L.y, L.z, L.w, R[2], R[3]);
+                            conv_mask_select(wv.z, L.x, L.y, L.z, L.w, R[4], R[5]);
+                            conv_mask_select(wv.w, L.x, L.y, L.z, L.w, R[6], R[7]);
+                            ptx::tmem_st_x8(ta + (q * 4 + j) * 8, R);
+                        }
                     }
                 }
                 ptx::tmem_wait_st();
-                ptx::tc_fence_before();
-                ptx::mbar_arrive(&afull[as]);
             }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&afull[as]);
+            ++i;
+        }
+        if (threadIdx.x == 256) {
+            FIREQ_TRACE_VAL(12, cw_full);
+            FIREQ_TRACE_VAL(13, cw_aempty);
+            FIREQ_TRACE_VAL(14, prof_clock() - ct0);
         }
     } else if (warp >= 4) {
         // ------------------------------------------------------- epilogue
+        ptx::pdl_wait();                    // beta, workspace and Y are shared with earlier kernels
         const int r = threadIdx.x & 127;
         const uint32_t lane_base = (uint32_t)(r & ~31) << 16;
         const float p2 = exp2_neg(a.pts_n);
         it.init(a, blockIdx.x);
         int sg = 0;
+        uint32_t fix_phase = 0;
         const long long u_first = (long long)blockIdx.x * a.U / a.C;
         while (it.next(tile, g0, g1)) {
             const int b = sg % ACCBUF;
@@ -365,35 +554,91 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
             }
             ptx::tc_fence_before();
             ptx::mbar_arrive(&accempty[b]);
+            if (r == 0) FIREQ_TRACE(6);
             if (!whole) {
                 // deterministic cross-CTA reduction: last arriver sums contributors in CTA order
-                __threadfence();
-                ptx::named_bar_sync(1, 128);
+                ptx::named_bar_sync(1, 128);         // all partial stores of this CTA issued
                 const long long t0 = (long long)tile * a.G, t1 = t0 + a.G - 1;
                 const int c_lo = owner_of(t0, a.U, a.C), c_hi = owner_of(t1, a.U, a.C);
                 if (r == 0) {
-                    const unsigned prev = atomicAdd(&a.counters[tile], 1u);
+                    // gpu-scope acq_rel: publishes this CTA's partials (bar.sync cumulativity)
+                    // and, for the last arriver, acquires everyone else's.
+                    unsigned prev;
+                    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&a.counters[tile]) : "memory");
                     misc[1] = (prev == (unsigned)(c_hi - c_lo)) ? 1u : 0u;
                 }
                 ptx::named_bar_sync(1, 128);
-                if (misc[1]) {
+                if (misc[1] && C::kFixSlots > 0) {
+                    // Stage the contributors' partials (contiguous kPartBytes blocks) into SMEM
+                    // with bulk copies, kFixSlots per round trip, and sum them in CTA order.
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    float accv[NTOK];
+#pragma unroll
+                    for (int c = 0; c < NTOK; ++c) accv[c] = 0.0f;
+                    for (int cc0 = c_lo; cc0 <= c_hi; cc0 += (C::kFixSlots > 0 ? C::kFixSlots : 1)) {
+                        const int nb = min(C::kFixSlots, c_hi - cc0 + 1);
+                        if (r < 32 && ptx::elect_one()) {
+                            ptx::mbar_arrive_expect_tx(fixbar, nb * C::kPartBytes);
+                            for (int q = 0; q < nb; ++q) {
+                                const int cc = cc0 + q;
+                                const long long cu0 = (long long)cc * a.U / a.C;
+                                const int sl = 2 * cc + ((cu0 < t0) ? 1 : 0);
+                                ptx::bulk_g2s(sFix + q * (C::kPartBytes / 4), a.partial + (size_t)sl * NTOK * kTileN,
+                                              C::kPartBytes, fixbar, 0ull);
+                            }
+                        }
+                        ptx::mbar_wait(fixbar, fix_phase);
+                        fix_phase ^= 1u;
+                        for (int q = 0; q < nb; ++q) {
+#pragma unroll
+                            for (int c = 0; c < NTOK; ++c)
+                                accv[c] = __fadd_rn(accv[c], sFix[q * (C::kPartBytes / 4) + c * kTileN + r]);
+                        }
+                        ptx::named_bar_sync(1, 128);      // sFix reuse
+                    }
+#pragma unroll
+                    for (int c = 0; c < NTOK; ++c) {
+                        const int m = m0 + c;
+                        if (m < a.M) {
+                            float y = __fmul_rn(accv[c], __fmul_rn(__bfloat162float(a.x_scale[m]), p2));
+                            if (a.gamma) y = __fmul_rn(y, gam);
+                            const __nv_bfloat16 yb = __float2bfloat16_rn(y);
+                            if (a.out_layout == 0) a.Y[(size_t)m * a.ldy + n] = yb;
+                            else a.Y[(size_t)n * a.ldy + m] = yb;
+                        }
+                    }
+                } else if (misc[1]) {
                     __threadfence();
 #pragma unroll 1
-                    for (int ch = 0; ch < NTOK / 16; ++ch) {
-                        float accv[16];
+                    for (int ch = 0; ch < NTOK / 8; ++ch) {
+                        float accv[8];
 #pragma unroll
-                        for (int c = 0; c < 16; ++c) accv[c] = 0.0f;
-                        for (int cc = c_lo; cc <= c_hi; ++cc) {
-                            const long long cu0 = (long long)cc * a.U / a.C;
-                            const int sl = 2 * cc + ((cu0 < t0) ? 1 : 0);
-                            const float* pp = a.partial + (size_t)sl * NTOK * kTileN;
+                        for (int c = 0; c < 8; ++c) accv[c] = 0.0f;
+                        // contributors in CTA order; loads of up to 4 contributors in flight
+                        for (int cc0 = c_lo; cc0 <= c_hi; cc0 += 4) {
+                            float tmp[4][8];
 #pragma unroll
-                            for (int c = 0; c < 16; ++c)
-                                accv[c] = __fadd_rn(accv[c], __ldcg(pp + (ch * 16 + c) * kTileN + r));
+                            for (int q = 0; q < 4; ++q) {
+                                const int cc = cc0 + q;
+                                if (cc <= c_hi) {
+                                    const long long cu0 = (long long)cc * a.U / a.C;
+                                    const int sl = 2 * cc + ((cu0 < t0) ? 1 : 0);
+                                    const float* pp = a.partial + (size_t)sl * NTOK * kTileN;
+#pragma unroll
+                                    for (int c = 0; c < 8; ++c) tmp[q][c] = __ldcg(pp + (ch * 8 + c) * kTileN + r);
+                                }
+                            }
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                if (cc0 + q <= c_hi) {
+#pragma unroll
+                                    for (int c = 0; c < 8; ++c) accv[c] = __fadd_rn(accv[c], tmp[q][c]);
+                                }
+                            }
                         }
 #pragma unroll
-                        for (int c = 0; c < 16; ++c) {
-                            const int m = m0 + ch * 16 + c;
+                        for (int c = 0; c < 8; ++c) {
+                            const int m = m0 + ch * 8 + c;
                             if (m < a.M) {
                                 float y = __fmul_rn(accv[c], __fmul_rn(__bfloat162float(a.x_scale[m]), p2));
                                 if (a.gamma) y = __fmul_rn(y, gam);
@@ -403,7 +648,10 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                             }
                         }
                     }
-                    if (r == 0) a.counters[tile] = 0u;   // leave the workspace zeroed
+                }
+                if (misc[1] && r == 0) {
+                    a.counters[tile] = 0u;           // leave the workspace zeroed
+                    FIREQ_TRACE(7);
                 }
                 ptx::named_bar_sync(1, 128);
             }
@@ -412,10 +660,12 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
     }
 
     // ------------------------------------------------------------ teardown
+    if (threadIdx.x == 128) FIREQ_TRACE(4);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     if (warp == 2) ptx::tmem_dealloc(tmem, C::kTmemCols);
+    if (threadIdx.x == 0) FIREQ_TRACE(5);
 }
 
 __global__ void k_lut_table(uint8_t* out) {
@@ -468,7 +718,7 @@ bool make_x_map(CUtensorMap* out, const uint8_t* x, int64_t M, int64_t K, int nt
 }
 
 struct Plan {
-    int ntok, m_tiles, n_tiles, tiles, G, mode, C;
+    int ntok, m_tiles, n_tiles, tiles, G, mode, C, R;
     long long U;
     bool sign_split;
 };
@@ -483,28 +733,32 @@ Plan make_plan(int64_t M, int64_t N, int64_t K) {
     p.G = (int)(K / kGroup);
     const int sms = sm_count();
     if (p.tiles >= 2 * sms) {
-        p.mode = 0;
+        // many tiles: whole tiles round-robin (last-wave imbalance < 1/2 of a tile per CTA)
+        p.R = 0;
         p.C = sms;
-        p.U = (long long)p.tiles * p.G;
     } else {
-        p.mode = 1;
-        p.U = (long long)p.tiles * p.G;
-        p.C = (int)std::min<long long>(sms, p.U);
+        // decode-sized: whole tiles for full waves, the remainder split over all CTAs
+        const int full_rounds = p.tiles / sms;
+        p.R = p.tiles - full_rounds * sms;
+        p.C = full_rounds > 0 ? sms : (int)std::min<long long>(sms, (long long)p.R * p.G);
     }
+    p.U = (long long)p.R * p.G;
+    p.mode = p.R > 0 ? 1 : 0;
     return p;
 }
 
-template <int NTOK, bool SS, int NCONV, int STAGES, int ASTAGES, int ACCBUF>
+template <int NTOK, bool SS, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS>
 fireq_status_t launch_cfg(const CUtensorMap& map, const GemmArgs& args, cudaStream_t stream) {
-    using C = Cfg<NTOK, SS, NCONV, STAGES, ASTAGES, ACCBUF>;
-    auto kern = k_w4a8_gemm<NTOK, SS, NCONV, STAGES, ASTAGES, ACCBUF>;
+    using C = Cfg<NTOK, SS, NCONV, STAGES, ASTAGES, ACCBUF, GPS>;
+    auto kern = k_w4a8_gemm<NTOK, SS, NCONV, STAGES, ASTAGES, ACCBUF, GPS>;
     static bool attr_done = false;
     if (!attr_done) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
             return fail(FIREQ_ERROR_CUDA, "cudaFuncSetAttribute(smem) failed");
         attr_done = true;
     }
-    kern<<<args.C, C::kThreads, C::kSmemBytes, stream>>>(map, args);
+    const cudaError_t e = launch_ex(kern, dim3(args.C), dim3(C::kThreads), C::kSmemBytes, stream, 1u, map, args);
+    if (e != cudaSuccess) return fail(FIREQ_ERROR_CUDA, std::string("fireq_w4a8_gemm launch: ") + cudaGetErrorString(e));
     return check_launch("fireq_w4a8_gemm");
 }
 
@@ -512,7 +766,7 @@ fireq_status_t launch_cfg(const CUtensorMap& map, const GemmArgs& args, cudaStre
 
 size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
     const Plan p = make_plan(M, N, K);
-    const size_t part = p.mode == 1 ? (size_t)2 * p.C * p.ntok * kTileN * sizeof(float) : 0;
+    const size_t part = p.R > 0 ? (size_t)2 * p.C * p.ntok * kTileN * sizeof(float) : 0;
     const size_t cnt = ((size_t)p.tiles * sizeof(unsigned) + 255) / 256 * 256;
     return cnt + part;
 }
@@ -548,15 +802,24 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
     args.n_tiles = p.n_tiles; args.m_tiles = p.m_tiles; args.tiles = p.tiles;
     args.pts_n = pts_n;
     args.out_layout = out_layout;
-    args.mode = p.mode;
+    args.R = p.R;
     args.C = p.C;
     args.U = p.U;
+    args.trace = g_trace;
+    {
+        static const int dbg = getenv("FIREQ_DEBUG_MODE") ? atoi(getenv("FIREQ_DEBUG_MODE")) : 0;
+        args.dbg = dbg;
+    }
     switch (p.ntok) {
-        case 16:  return launch_cfg<16, true, 2, 16, 4, 2>(map, args, stream);
-        case 32:  return launch_cfg<32, true, 2, 14, 4, 2>(map, args, stream);
-        case 64:  return launch_cfg<64, true, 2, 10, 4, 2>(map, args, stream);
-        case 128: return launch_cfg<128, true, 2, 7, 4, 2>(map, args, stream);
-        default:  return launch_cfg<256, false, 2, 4, 4, 1>(map, args, stream);
+        // <NTOK, sign-split, converter WGs, SMEM stages, TMEM A stages, accumulators, groups/stage>
+        // decode configs: >= 128 KB of weights in flight per SM (hides the loaded DRAM
+        // latency), 2 groups per stage (halves the per-stage synchronisation cost), and
+        // <= 96 registers per thread so a CTA of the next small kernel of a PDL chain fits.
+        case 16:  return launch_cfg<16, true, 3, 8, 3, 2, 2>(map, args, stream);
+        case 32:  return launch_cfg<32, true, 3, 7, 3, 2, 2>(map, args, stream);
+        case 64:  return launch_cfg<64, true, 2, 5, 2, 2, 2>(map, args, stream);
+        case 128: return launch_cfg<128, true, 2, 7, 4, 2, 1>(map, args, stream);
+        default:  return launch_cfg<256, false, 2, 4, 4, 1, 1>(map, args, stream);
     }
 }
 

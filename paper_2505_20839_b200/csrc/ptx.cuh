@@ -129,6 +129,13 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 }
 
 // ------------------------------------------------------------------ misc
+// One lane of a converged warp returns true (PTX elect.sync).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P1;\n\telect.sync _|P1, 0xffffffff;\n\tselp.b32 %0, 1, 0, P1;\n\t}"
+                 : "=r"(pred));
+    return pred != 0;
+}
 // Generic-mode byte permute: selector nibble bit 3 = replicate the msb of the
 // selected byte (CUDA's __byte_perm masks selectors to 3 bits, so use PTX).
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -152,6 +159,34 @@ __device__ __forceinline__ uint32_t shl4_fma(uint32_t x) {
     uint32_t d;
     asm("mul.lo.u32 %0, %1, 16;" : "=r"(d) : "r"(x));
     return d;
+}
+// Programmatic dependent launch (PDL): let the next kernel in the stream start its
+// prologue now / wait until the previous kernel has completed and flushed memory.
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+// Thread-block cluster helpers (DSMEM).
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Map a local shared address to the same offset in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ float ld_shared_cluster_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
 }
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

@@ -1,9 +1,13 @@
 // quant_act.cu -- fireq_quantize_act (A1..A3, Eq. 2, per token P:482) and the
 // FFN helper fireq_silu_mul_quantize_act (SiLU * up, then A2..A3).
 //
-// One CTA per token row; the row is read twice (amax pass, encode pass; the second
-// pass hits L1/L2).  Memory-bound: 2 B read + 1 B written per element.
+// Each token row is split over a cluster of CL CTAs (CL = 8 at decode sizes); the
+// chunk is read twice (amax pass, encode pass; the second pass hits L1).
+// Memory-bound: 2 B read + 1 B written per element.  Launched with PDL.
+#include <algorithm>
+
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace fireq {
 namespace {
@@ -56,27 +60,48 @@ __device__ __forceinline__ void load8(const Src& s, int64_t row_off, int64_t k, 
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_act_quant(Src s, int64_t K, int64_t ld,
+// Grid (CL, M), cluster (CL, 1, 1): CTA `rank` of a cluster quantizes columns
+// [rank*K/CL, (rank+1)*K/CL) of token row m; the row amax is combined across the
+// cluster through distributed shared memory (DSMEM).  CL = 8 for decode-sized M
+// (spreads a 16-token batch over 128 CTAs), 1 for large M.
+__global__ void __launch_bounds__(kThreads) k_act_quant(Src s, int64_t M, int64_t K, int64_t ld, int cl,
                                                         uint8_t* __restrict__ xq,
                                                         __nv_bfloat16* __restrict__ beta_out) {
     __shared__ float red[32];
-    const int64_t m = blockIdx.x;
+    ptx::pdl_trigger();
+    ptx::pdl_wait();                       // X / G / U come from the previous kernel
+    const int rank = cl > 1 ? (int)ptx::cluster_ctarank() : 0;
+    for (int64_t m = blockIdx.y; m < M; m += gridDim.y) {
     const int64_t row_off = m * ld;
+    const int64_t chunk = K / cl;
+    const int64_t k0 = rank * chunk, k1 = k0 + chunk;
     float amax = 0.0f;
-    for (int64_t k = (int64_t)threadIdx.x * 8; k < K; k += kThreads * 8) {
+    for (int64_t k = k0 + (int64_t)threadIdx.x * 8; k < k1; k += kThreads * 8) {
         float v[8];
         load8(s, row_off, k, v);
 #pragma unroll
         for (int i = 0; i < 8; ++i) amax = fmaxf(amax, fabsf(v[i]));
     }
-    amax = block_max(amax, red);
+    amax = block_max(amax, red);           // red[0] = this CTA's max
+    if (cl > 1) {
+        ptx::cluster_sync();               // every CTA's red[0] is written
+        if (threadIdx.x < 32) {
+            float v = 0.0f;
+            if (threadIdx.x < (unsigned)cl)
+                v = ptx::ld_shared_cluster_f32(ptx::mapa_shared(ptx::smem_u32(&red[0]), threadIdx.x));
+            for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+            if (threadIdx.x == 0) red[1] = v;
+        }
+        ptx::cluster_sync();               // remote reads done before any CTA moves on / exits
+        amax = red[1];
+    }
     // A2: beta = bf16_RN(amax / 448) (fp32 division then RNE; equals exact RNE for bf16 operands)
     const __nv_bfloat16 beta_h = amax > 0.0f ? __float2bfloat16_rn(__fdiv_rn(amax, 448.0f))
                                              : __float2bfloat16_rn(1.0f);
     const float beta = __bfloat162float(beta_h);
-    if (threadIdx.x == 0) beta_out[m] = beta_h;
+    if (threadIdx.x == 0 && rank == 0) beta_out[m] = beta_h;
     // A3: x_hat = E4M3_RN_satfinite(x' / beta)
-    for (int64_t k = (int64_t)threadIdx.x * 8; k < K; k += kThreads * 8) {
+    for (int64_t k = k0 + (int64_t)threadIdx.x * 8; k < k1; k += kThreads * 8) {
         float v[8];
         load8(s, row_off, k, v);
         uint2 o;
@@ -86,6 +111,8 @@ __global__ void __launch_bounds__(kThreads) k_act_quant(Src s, int64_t K, int64_
               (e4m3x2_rn(__fdiv_rn(v[6], beta), __fdiv_rn(v[7], beta)) << 16);
         *reinterpret_cast<uint2*>(xq + m * K + k) = o;
     }
+    __syncthreads();                       // red[] reuse by the next row
+    }
 }
 
 }  // namespace
@@ -94,7 +121,11 @@ fireq_status_t quantize_act_impl(const __nv_bfloat16* X, const __nv_bfloat16* U,
                                  int64_t ld, const __nv_bfloat16* c, int mode, uint8_t* xq,
                                  __nv_bfloat16* beta, cudaStream_t stream) {
     Src s{X, U, c, mode};
-    k_act_quant<<<(unsigned)M, kThreads, 0, stream>>>(s, K, ld, xq, beta);
+    const int cl = M <= 64 ? 8 : 1;
+    const unsigned rows = (unsigned)std::min<int64_t>(M, 65535);
+    const cudaError_t e = launch_ex(k_act_quant, dim3((unsigned)cl, rows), dim3(kThreads), 0, stream,
+                                    (unsigned)cl, s, M, K, ld, cl, xq, beta);
+    if (e != cudaSuccess) return fail(FIREQ_ERROR_CUDA, std::string("act quant launch: ") + cudaGetErrorString(e));
     return check_launch(mode == 2 ? "fireq_silu_mul_quantize_act" : "fireq_quantize_act");
 }
 

@@ -21,7 +21,7 @@ EXPORTS = [
     "fireq_quantize_weight_workspace_bytes", "fireq_w4a8_gemm_workspace_bytes",
     "fireq_quantize_weight", "fireq_quantize_act", "fireq_silu_mul_quantize_act",
     "fireq_w4a8_gemm", "fireq_comm_get_unique_id", "fireq_comm_init", "fireq_comm_destroy",
-    "fireq_w4a8_gemm_colpar", "fireq_debug_lut_table", "fireq_gemm_plan",
+    "fireq_w4a8_gemm_colpar", "fireq_debug_lut_table", "fireq_gemm_plan", "fireq_debug_set_trace",
 ]
 
 
@@ -56,6 +56,7 @@ def load(path=LIB_PATH):
         "fireq_w4a8_gemm_colpar": ([P, P, I64, I64, P, P, I64, I32, P, P, SZ, P, P], C),
         "fireq_debug_lut_table": ([P, P], C),
         "fireq_gemm_plan": ([I64, I64, I64, P], C),
+        "fireq_debug_set_trace": ([P], C),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -204,6 +205,11 @@ def w4a8_gemm(xq, beta, packed, scales, N, pts_n, gamma=None, out=None, out_layo
     _check(L.fireq_w4a8_gemm(_ptr(xq), _ptr(beta), M, K, _ptr(packed), _ptr(scales), N, pts_n, _ptr(gamma),
                              _ptr(out), ldy, out_layout, _ptr(ws), ws.numel(), _stream(stream)), "fireq_w4a8_gemm")
     return out
+
+
+def debug_set_trace(buf):
+    """buf: uint64 CUDA tensor [ctas*8] or None."""
+    _check(lib().fireq_debug_set_trace(_ptr(buf) if buf is not None else None), "fireq_debug_set_trace")
 
 
 def debug_lut_table(device="cuda"):
