@@ -87,9 +87,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #if FIREQ_PROFILE
 #define FIREQ_TRACE(slot) do { if (a.trace) a.trace[blockIdx.x * 16 + (slot)] = gtimer(); } while (0)
 #define FIREQ_TRACE_VAL(slot, v) do { if (a.trace) a.trace[blockIdx.x * 16 + (slot)] = (v); } while (0)
+// per-stage event log of CTA 0: trace[C*16 + stage*8 + ev] (first 64 stages)
+#define FIREQ_EVT(stage, ev) do { if (a.trace && blockIdx.x == 0 && (stage) < 64) \
+    a.trace[a.C * 16 + (stage) * 8 + (ev)] = clock64(); } while (0)
 #else
 #define FIREQ_TRACE(slot) do { } while (0)
 #define FIREQ_TRACE_VAL(slot, v) do { } while (0)
+#define FIREQ_EVT(stage, ev) do { } while (0)
 #endif
 
 // Segment = contiguous run of groups [g0, g1) of one tile processed by one CTA.
@@ -176,14 +180,15 @@ __host__ __device__ constexpr uint32_t make_idesc(int ntok, bool negate_a) {
          | ((uint32_t)(128 >> 4) << 24);      // M >> 4
 }
 
-template <int NTOK, bool SIGN_SPLIT, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS>
+template <int NTOK, bool SIGN_SPLIT, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS, int NMMA>
 struct Cfg {
     static constexpr int kXBytes = NTOK * kGroup;                       // FP8 activation tile (1 group)
     static constexpr int kXStage = GPS * kXBytes;
     static constexpr int kWStage = GPS * kWBytes;
     static constexpr int kSStage = GPS * kTileN;
     static constexpr int kASz = GPS * (SIGN_SPLIT ? 64 : 32);           // TMEM cols per A stage
-    static constexpr int kAccCols = ACCBUF * NTOK;
+    // accumulator (buffer b, issuer w) at TMEM columns [(b * NMMA + w) * NTOK, ... + NTOK)
+    static constexpr int kAccCols = ACCBUF * NMMA * NTOK;
     static constexpr int kACol0 = (kAccCols + 31) / 32 * 32;
     static constexpr int kTmemNeed = kACol0 + ASTAGES * kASz;
     static constexpr int kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128
@@ -267,13 +272,13 @@ __device__ __forceinline__ void conv_mask_select(uint32_t w, uint32_t L0, uint32
     r1 = ptx::lop3_mux(ptx::prmt(L0, L1, wh), ptx::prmt(L2, L3, xh), m1);
 }
 
-// Roles (warp-uniform): warp 0 = weight TMA producer, warp 1 = MMA issuer, warp 2 =
-// TMEM allocator, warp 3 = activation TMA producer (the only producer that waits on
-// the previous kernel, PDL), warps 4-7 = epilogue, warps 8.. = converter warpgroups.
-template <int NTOK, bool SIGN_SPLIT, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS>
+// Roles (warp-uniform, see kW* below): converter warpgroups, epilogue warpgroup, TMEM
+// allocator, activation TMA producer (the only role that waits on the previous kernel,
+// PDL), weight TMA producer, MMA issuer.
+template <int NTOK, bool SIGN_SPLIT, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS, int NMMA>
 __global__ void __maxnreg__((NTOK <= 32 ? 88 : NTOK <= 64 ? 96 : 128))
 k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
-    using C = Cfg<NTOK, SIGN_SPLIT, NCONV, STAGES, ASTAGES, ACCBUF, GPS>;
+    using C = Cfg<NTOK, SIGN_SPLIT, NCONV, STAGES, ASTAGES, ACCBUF, GPS, NMMA>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment for the SW128 tiles, computed on the shared-window address so
     // that the pointer stays visibly in the shared state space (LDS, not generic LD).
@@ -296,31 +301,40 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    // Warp roles.  The SM warp scheduler favours higher warp ids, so the latency-critical
+    // single-warp roles take the highest ids and the throughput-bound converters the lowest
+    // (otherwise the converters starve the MMA issuer and the TMA producers).
+    constexpr int kWEpi = 4 * NCONV;            // epilogue warpgroup: warps kWEpi .. kWEpi+3
+    constexpr int kWAlloc = kWEpi + 4;          // TMEM allocator, LUT builder
+    constexpr int kWProdX = kWEpi + 5;          // activation TMA producer (waits on PDL), LUT builder
+    constexpr int kWProdW = kWEpi + 6;          // weight TMA producer
+    constexpr int kWMma = kWEpi + 7;            // MMA issuer
 
     // ------------------------------------------------------------ setup
     if (threadIdx.x == 0) FIREQ_TRACE(0);
-    if (warp == 0) ptx::pdl_trigger();      // the next kernel may start its prologue
-    if (warp == 0 && lane == 0) {
+    if (warp == kWProdW) ptx::pdl_trigger();   // the next kernel may start its prologue
+    if (warp == kWProdW && lane == 0) {
         for (int i = 0; i < STAGES; ++i) {
-            ptx::mbar_init(&fullW[i], 1);
+            ptx::mbar_init(&fullW[i], 2);       // weight producer + activation producer
             ptx::mbar_init(&fullX[i], 1);
             ptx::mbar_init(&empty[i], 1);
         }
-        for (int i = 0; i < ASTAGES; ++i) { ptx::mbar_init(&afull[i], 128); ptx::mbar_init(&aempty[i], 1); }
-        for (int i = 0; i < ACCBUF; ++i) { ptx::mbar_init(&accfull[i], 1); ptx::mbar_init(&accempty[i], 128); }
+        // afull / accempty: one arrival per warp of the 4-warp group (after __syncwarp)
+        for (int i = 0; i < ASTAGES; ++i) { ptx::mbar_init(&afull[i], 4); ptx::mbar_init(&aempty[i], 1); }
+        for (int i = 0; i < ACCBUF; ++i) { ptx::mbar_init(&accfull[i], NMMA); ptx::mbar_init(&accempty[i], 4); }
         ptx::mbar_init(fixbar, 1);
         ptx::fence_mbar_init();
         ptx::prefetch_tmap(&tmap_x);
     }
-    if (warp == 2) {
+    if (warp == kWAlloc) {
         ptx::tmem_alloc(&misc[0], C::kTmemCols);
         ptx::tmem_relinquish();
     }
-    if (warp == 2 || warp == 3) {
+    if (warp == kWAlloc || warp == kWProdX) {
         // LUT-of-LUTs: entry [s][u] = E4M3_RN(v(u) * sigma_s) for all 127 finite sigma codes
         // (Step 1's 16-entry table).  v * sigma is exact in fp32.
         uint8_t* lut = reinterpret_cast<uint8_t*>(sLut);
-        for (int e = threadIdx.x - 64; e < kLutEntries; e += 64) {
+        for (int e = threadIdx.x - kWAlloc * 32; e < kLutEntries; e += 64) {
             const int s = e >> 4, u = e & 15;
             const float v = (float)(u < 8 ? u : u - 16);
             lut[e] = (uint8_t)e4m3_rn(__fmul_rn(v, e4m3_decode((uint32_t)s)));
@@ -338,7 +352,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
     int nt, mt, g, ng;
     bool sfirst, slast;
 
-    if (warp == 0) {
+    if (warp == kWProdW) {
         // ------------------------------------------------------- weight producer
         // Weights never depend on the previous kernel, so this warp streams them from
         // the start (PDL overlap); the whole warp walks the schedule and one elected
@@ -349,6 +363,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
         while (st.next(nt, mt, g, ng, sfirst, slast)) {
             const int s = i % STAGES;
             ptx::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+            if (lane == 0) FIREQ_EVT(i, 0);
             if (ptx::elect_one()) {
                 if (a.dbg & 4) {
                     ptx::mbar_arrive(&fullW[s]);
@@ -362,7 +377,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
             __syncwarp();
             ++i;
         }
-    } else if (warp == 3) {
+    } else if (warp == kWProdX) {
         // ------------------------------------------------------- activation producer
         const uint64_t pol_x = ptx::policy_evict_last();    // activations: re-read by every tile
         ptx::pdl_wait();                    // activations are written by the previous kernel
@@ -373,76 +388,96 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
             ptx::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
             if (ptx::elect_one()) {
                 if (a.dbg & 4) {
-                    ptx::mbar_arrive(&fullX[s]);
+                    ptx::mbar_arrive(&fullW[s]);
                 } else {
-                    ptx::mbar_arrive_expect_tx(&fullX[s], ng * C::kXBytes);
+                    // same barrier as the weights (arrival count 2): the converters wait on it,
+                    // and the MMA issuer, which waits on the converters, needs no extra wait.
+                    ptx::mbar_arrive_expect_tx(&fullW[s], ng * C::kXBytes);
                     for (int q = 0; q < ng; ++q)
                         ptx::tma_2d_g2s(sX + s * C::kXStage + q * C::kXBytes, &tmap_x, (g + q) * kGroup, mt * NTOK,
-                                        &fullX[s], pol_x);
+                                        &fullW[s], pol_x);
                 }
             }
             __syncwarp();
             ++i;
         }
-    } else if (warp == 1) {
-        // ------------------------------------------------------- MMA issuer
+    } else if (warp == kWMma || (NMMA == 2 && warp == kWAlloc)) {
+        // ------------------------------------------------------- MMA issuer(s)
         // Whole warp walks the schedule; one elected lane issues the stage's MMAs back to
-        // back and the commits (see the producer comment about waterfall loops).
+        // back and the commits (see the producer comment about waterfall loops).  With
+        // NMMA = 2 two warps issue alternate stages into separate accumulators (the
+        // epilogue adds them): at decode sizes the MMAs are short and one issuing warp
+        // cannot keep the tensor pipe busy.
+        const int w = (warp == kWMma) ? 0 : 1;
         constexpr uint32_t idesc_pos = make_idesc(NTOK, false);
         constexpr uint32_t idesc_neg = make_idesc(NTOK, true);
         st.init(a, blockIdx.x);
         int i = 0, sg = 0;
         const uint32_t sx0 = ptx::smem_u32(sX);
         uint32_t d = tmem;
+        bool touched = false;
         long long w_afull = 0, w_full = 0, t_issue = 0, t_mma0 = prof_clock();
         while (st.next(nt, mt, g, ng, sfirst, slast)) {
-            const int s = i % STAGES, as = i % ASTAGES;
+            const int b = sg % ACCBUF;
             if (sfirst) {
-                const int b = sg % ACCBUF;
                 ptx::mbar_wait(&accempty[b], ((sg / ACCBUF) & 1) ^ 1);
-                d = tmem + b * NTOK;
+                d = tmem + (b * NMMA + w) * NTOK;
+                touched = false;
             }
-            const long long c0 = prof_clock();
-            ptx::mbar_wait(&afull[as], (i / ASTAGES) & 1);
-            const long long c1 = prof_clock();
-            ptx::mbar_wait(&fullX[s], (i / STAGES) & 1);
-            w_afull += c1 - c0;
-            w_full += prof_clock() - c1;
-            ptx::tc_fence_after();
-            const uint32_t ta = tmem + C::kACol0 + as * C::kASz;
-            const long long c2 = prof_clock();
-            if (ptx::elect_one()) {
-                if (!(a.dbg & 2)) {
-                    for (int q = 0; q < ng; ++q) {
-                        const uint64_t bdesc = smem_desc_sw128(sx0 + s * C::kXStage + q * C::kXBytes);
+            if ((i % NMMA) == w) {
+                const int s = i % STAGES, as = i % ASTAGES;
+                const long long c0 = prof_clock();
+                ptx::mbar_wait(&afull[as], (i / ASTAGES) & 1);
+                if (lane == 0) FIREQ_EVT(i, 4);
+                const long long c1 = prof_clock();
+                if (lane == 0) FIREQ_EVT(i, 5);
+                w_afull += c1 - c0;
+                w_full += prof_clock() - c1;
+                ptx::tc_fence_after();
+                const uint32_t ta = tmem + C::kACol0 + as * C::kASz;
+                const long long c2 = prof_clock();
+                if (ptx::elect_one()) {
+                    if (!(a.dbg & 2)) {
+                        for (int q = 0; q < ng; ++q) {
+                            const uint64_t bdesc = smem_desc_sw128(sx0 + s * C::kXStage + q * C::kXBytes);
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const uint64_t bd = bdesc + (uint64_t)(j * 32 >> 4);   // +32 B along K
-                            const uint32_t acc = (sfirst && q == 0 && j == 0) ? 0u : 1u;
-                            ptx::mma_f8f6f4_ts(d, ta + (q * 4 + j) * 8, bd, idesc_pos, acc);
-                            if (SIGN_SPLIT)
-                                ptx::mma_f8f6f4_ts(d, ta + GPS * 32 + (q * 4 + j) * 8, bd, idesc_neg, 1u);
+                            for (int j = 0; j < 4; ++j) {
+                                const uint64_t bd = bdesc + (uint64_t)(j * 32 >> 4);   // +32 B along K
+                                const uint32_t acc = (!touched && q == 0 && j == 0) ? 0u : 1u;
+                                ptx::mma_f8f6f4_ts(d, ta + (q * 4 + j) * 8, bd, idesc_pos, acc);
+                                if (SIGN_SPLIT)
+                                    ptx::mma_f8f6f4_ts(d, ta + GPS * 32 + (q * 4 + j) * 8, bd, idesc_neg, 1u);
+                            }
                         }
                     }
+                    ptx::mma_commit(&empty[s]);
                 }
-                ptx::mma_commit(&empty[s]);
-                if (slast) ptx::mma_commit(&accfull[sg % ACCBUF]);
+                __syncwarp();
+                touched = true;
+                t_issue += prof_clock() - c2;
+                if (lane == 0) FIREQ_EVT(i, 6);
             }
-            __syncwarp();
-            t_issue += prof_clock() - c2;
-            if (slast) ++sg;
+            if (slast) {
+                // accfull completes when every issuer has committed (or had no stage)
+                if (ptx::elect_one()) {
+                    if (touched) ptx::mma_commit(&accfull[b]);
+                    else ptx::mbar_arrive(&accfull[b]);
+                }
+                __syncwarp();
+                ++sg;
+            }
             ++i;
         }
-        if (lane == 0) {
+        if (lane == 0 && w == 0) {
             FIREQ_TRACE(3);
             FIREQ_TRACE_VAL(9, w_afull);
             FIREQ_TRACE_VAL(10, w_full);
             FIREQ_TRACE_VAL(11, prof_clock() - t_mma0);
             FIREQ_TRACE_VAL(15, t_issue);
         }
-    } else if (warp >= 8) {
+    } else if (warp < kWEpi) {
         // ------------------------------------------------------- converters
-        const int wg = (warp - 8) >> 2;           // converter warpgroup
+        const int wg = warp >> 2;                 // converter warpgroup
         const int r = threadIdx.x & 127;          // weight row == TMEM lane
         const uint32_t lane_base = (uint32_t)(r & ~31) << 16;
         st.init(a, blockIdx.x);
@@ -454,7 +489,8 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
             const long long c0 = prof_clock();
             ptx::mbar_wait(&fullW[s], (i / STAGES) & 1);
             cw_full += prof_clock() - c0;
-            if (i == 0 && threadIdx.x == 256) FIREQ_TRACE(2);
+            if (r == 0) FIREQ_EVT(i, 1);
+            if (i == 0 && threadIdx.x == 0) FIREQ_TRACE(2);
             const long long c1 = prof_clock();
             if (i >= ASTAGES) {
                 // A stage `as` was last read by the MMAs of stage i - ASTAGES, whose commit
@@ -465,6 +501,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                 ptx::mbar_wait(&empty[j % STAGES], (j / STAGES) & 1);
             }
             cw_aempty += prof_clock() - c1;
+            if (r == 0) FIREQ_EVT(i, 2);
             ptx::tc_fence_after();
             if (!(a.dbg & 1)) {
                 const uint32_t ta = tmem + lane_base + C::kACol0 + as * C::kASz;
@@ -500,26 +537,34 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                 ptx::tmem_wait_st();
             }
             ptx::tc_fence_before();
-            ptx::mbar_arrive(&afull[as]);
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&afull[as]);
+            if (r == 0) FIREQ_EVT(i, 3);
             ++i;
         }
-        if (threadIdx.x == 256) {
+        if (threadIdx.x == 0) {
             FIREQ_TRACE_VAL(12, cw_full);
             FIREQ_TRACE_VAL(13, cw_aempty);
             FIREQ_TRACE_VAL(14, prof_clock() - ct0);
         }
-    } else if (warp >= 4) {
+    } else if (warp < kWEpi + 4) {
         // ------------------------------------------------------- epilogue
         ptx::pdl_wait();                    // beta, workspace and Y are shared with earlier kernels
         const int r = threadIdx.x & 127;
         const uint32_t lane_base = (uint32_t)(r & ~31) << 16;
         const float p2 = exp2_neg(a.pts_n);
         it.init(a, blockIdx.x);
-        int sg = 0;
+        int sg = 0, i_stage = 0;
         uint32_t fix_phase = 0;
         const long long u_first = (long long)blockIdx.x * a.U / a.C;
         while (it.next(tile, g0, g1)) {
             const int b = sg % ACCBUF;
+            // with NMMA issuers, accumulator w holds the stages i of this segment with
+            // i % NMMA == w; a one-stage segment only touched the first stage's issuer.
+            const int nstages = (g1 - g0 + GPS - 1) / GPS;
+            const int w_first = i_stage % NMMA;
+            const bool both = NMMA == 2 && nstages >= 2;
+            i_stage += nstages;
             ptx::mbar_wait(&accfull[b], (sg / ACCBUF) & 1);
             ptx::tc_fence_after();
             const int ntile = tile % a.n_tiles, mtile = tile / a.n_tiles;
@@ -533,8 +578,18 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
 #pragma unroll 1
             for (int ch = 0; ch < NTOK / 16; ++ch) {
                 uint32_t v[16];
-                ptx::tmem_ld_x16(tmem + lane_base + b * NTOK + ch * 16, v);
-                ptx::tmem_wait_ld();
+                ptx::tmem_ld_x16(tmem + lane_base + (b * NMMA + w_first) * NTOK + ch * 16, v);
+                if (both) {
+                    uint32_t v2[16];
+                    ptx::tmem_ld_x16(tmem + lane_base + (b * NMMA + (w_first ^ 1)) * NTOK + ch * 16, v2);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < 16; ++c)   // fixed order: issuer 0 + issuer 1
+                        v[c] = __float_as_uint(w_first == 0 ? __fadd_rn(__uint_as_float(v[c]), __uint_as_float(v2[c]))
+                                                            : __fadd_rn(__uint_as_float(v2[c]), __uint_as_float(v[c])));
+                } else {
+                    ptx::tmem_wait_ld();
+                }
                 if (whole) {
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
@@ -553,7 +608,8 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                 }
             }
             ptx::tc_fence_before();
-            ptx::mbar_arrive(&accempty[b]);
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&accempty[b]);
             if (r == 0) FIREQ_TRACE(6);
             if (!whole) {
                 // deterministic cross-CTA reduction: last arriver sums contributors in CTA order
@@ -660,11 +716,11 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
     }
 
     // ------------------------------------------------------------ teardown
-    if (threadIdx.x == 128) FIREQ_TRACE(4);
+    if (threadIdx.x == kWEpi * 32) FIREQ_TRACE(4);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    if (warp == 2) ptx::tmem_dealloc(tmem, C::kTmemCols);
+    if (warp == kWAlloc) ptx::tmem_dealloc(tmem, C::kTmemCols);
     if (threadIdx.x == 0) FIREQ_TRACE(5);
 }
 
@@ -747,10 +803,10 @@ Plan make_plan(int64_t M, int64_t N, int64_t K) {
     return p;
 }
 
-template <int NTOK, bool SS, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS>
+template <int NTOK, bool SS, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS, int NMMA>
 fireq_status_t launch_cfg(const CUtensorMap& map, const GemmArgs& args, cudaStream_t stream) {
-    using C = Cfg<NTOK, SS, NCONV, STAGES, ASTAGES, ACCBUF, GPS>;
-    auto kern = k_w4a8_gemm<NTOK, SS, NCONV, STAGES, ASTAGES, ACCBUF, GPS>;
+    using C = Cfg<NTOK, SS, NCONV, STAGES, ASTAGES, ACCBUF, GPS, NMMA>;
+    auto kern = k_w4a8_gemm<NTOK, SS, NCONV, STAGES, ASTAGES, ACCBUF, GPS, NMMA>;
     static bool attr_done = false;
     if (!attr_done) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
@@ -811,15 +867,16 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
         args.dbg = dbg;
     }
     switch (p.ntok) {
-        // <NTOK, sign-split, converter WGs, SMEM stages, TMEM A stages, accumulators, groups/stage>
+        // <NTOK, sign-split, converter WGs, SMEM stages, TMEM A stages, accumulators, groups/stage,
+        //  MMA-issuing warps>
         // decode configs: >= 128 KB of weights in flight per SM (hides the loaded DRAM
         // latency), 2 groups per stage (halves the per-stage synchronisation cost), and
         // <= 96 registers per thread so a CTA of the next small kernel of a PDL chain fits.
-        case 16:  return launch_cfg<16, true, 3, 8, 3, 2, 2>(map, args, stream);
-        case 32:  return launch_cfg<32, true, 3, 7, 3, 2, 2>(map, args, stream);
-        case 64:  return launch_cfg<64, true, 2, 5, 2, 2, 2>(map, args, stream);
-        case 128: return launch_cfg<128, true, 2, 7, 4, 2, 1>(map, args, stream);
-        default:  return launch_cfg<256, false, 2, 4, 4, 1, 1>(map, args, stream);
+        case 16:  return launch_cfg<16, true, 3, 8, 3, 2, 2, 2>(map, args, stream);
+        case 32:  return launch_cfg<32, true, 3, 7, 3, 2, 2, 1>(map, args, stream);
+        case 64:  return launch_cfg<64, true, 2, 5, 2, 2, 2, 1>(map, args, stream);
+        case 128: return launch_cfg<128, true, 2, 7, 4, 2, 1, 1>(map, args, stream);
+        default:  return launch_cfg<256, false, 2, 4, 4, 1, 1, 1>(map, args, stream);
     }
 }
 
