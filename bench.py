@@ -300,8 +300,7 @@ def run_fireq(args, rank, world, dev):
     F.load()
     peaks, peak_src = load_peaks()
     stream = torch.cuda.Stream(device=dev)
-    barrier = (lambda: torch.distributed.barrier()) if world > 1 else None
-    if world > 1:
+    if world > 1 or args.colpar:
         from paper_2505_20839_b200 import multigpu
         return multigpu.run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src)
 
@@ -451,6 +450,7 @@ def main():
     ap.add_argument("--impl", choices=["fireq", "reference"], default="fireq")
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--colpar", action="store_true", help="column-parallel path even at N=1 (testing)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -462,12 +462,17 @@ def main():
         raise SystemExit("bench.py --impl fireq needs a CUDA device (no CPU fallback)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    dist_on = world > 1 or args.colpar
+    if dist_on:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         torch.distributed.init_process_group("nccl", device_id=dev)
     try:
         run_fireq(args, rank, world, dev)
     finally:
-        if world > 1:
+        if dist_on:
             torch.distributed.destroy_process_group()
 
 

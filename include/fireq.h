@@ -138,6 +138,19 @@ fireq_status_t fireq_silu_mul_quantize_act(const void* G, const void* U, int64_t
                                            int64_t ld, uint8_t* x_fp8, void* x_scale,
                                            void* stream);
 
+/*
+ * Transposed-input variants (the Y^T layout produced by the column-parallel GEMM and
+ * its in-place all-gather): element (m, k) of the activation is read from
+ * Xt[k * ldt + m] (Xt is [K][ldt], ldt >= M).  Same arithmetic and outputs
+ * (x_fp8 [M][K] row-major, x_scale [M]) as the row-major functions above.
+ */
+fireq_status_t fireq_quantize_act_t(const void* Xt, int64_t M, int64_t K, int64_t ldt,
+                                    const void* chan_mul, uint8_t* x_fp8, void* x_scale,
+                                    void* stream);
+fireq_status_t fireq_silu_mul_quantize_act_t(const void* Gt, const void* Ut, int64_t M, int64_t K,
+                                             int64_t ldt, uint8_t* x_fp8, void* x_scale,
+                                             void* stream);
+
 /* ------------------------------------------------------------------ GEMM */
 /*
  * fireq_w4a8_gemm -- Steps 1..3 of the INT4 x FP8 kernel:
@@ -178,17 +191,19 @@ fireq_status_t fireq_comm_destroy(fireq_comm_t comm);
  * fireq_w4a8_gemm_colpar -- column-parallel (N-sharded) linear layer
  * (BASELINE north_star (d)): this rank holds rows [rank*N_local, (rank+1)*N_local)
  * of the quantized weight (byte slices of the full packing, layout v1, because
- * CAS lambda and PTS n are computed on the full tensor before sharding).  X is
- * replicated.  The rank computes its slice with fireq_w4a8_gemm in the Y^T
- * layout directly into its slot of Yt_full [N_local*nranks][M] and an in-place
- * ncclAllGather (bf16) over NVLink completes Y^T on every rank, on `stream`.
- *   Yt_full   out bf16 [nranks*N_local][M] (Y^T, ld = M).
+ * CAS lambda and PTS n are computed on the full tensor before sharding; a shard
+ * may end in zero-padded rows so that all shards have equal N_local, a multiple
+ * of 128).  X is replicated.  The rank computes its slice with fireq_w4a8_gemm in
+ * the Y^T layout directly into its slot of Yt_full [N_local*nranks][M] and an
+ * in-place ncclAllGather (bf16) over NVLink completes Y^T on every rank, on `stream`.
+ *   out_chan_scale_local  float [N_local] gamma for this shard's rows, or NULL.
+ *   Yt_full   out bf16 [nranks*N_local][M] (Y^T, ld = M; M % 8 == 0).
  */
 fireq_status_t fireq_w4a8_gemm_colpar(const uint8_t* x_fp8, const void* x_scale, int64_t M,
                                       int64_t K, const uint8_t* w_packed_local,
                                       const uint8_t* w_scales_local, int64_t N_local,
-                                      int32_t pts_exponent, void* Yt_full,
-                                      void* workspace, size_t workspace_bytes,
+                                      int32_t pts_exponent, const float* out_chan_scale_local,
+                                      void* Yt_full, void* workspace, size_t workspace_bytes,
                                       fireq_comm_t comm, void* stream);
 
 /* --------------------------------------------------------- introspection */

@@ -17,8 +17,8 @@ fireq_status_t quantize_weight_impl(const __nv_bfloat16* W, int64_t N, int64_t K
                                     int32_t* pts_and_status, void* ws, cudaStream_t stream);
 size_t wq_workspace_bytes(int64_t K);
 fireq_status_t quantize_act_impl(const __nv_bfloat16* X, const __nv_bfloat16* U, int64_t M, int64_t K, int64_t ld,
-                                 const __nv_bfloat16* c, int mode, uint8_t* xq, __nv_bfloat16* beta,
-                                 cudaStream_t stream);
+                                 const __nv_bfloat16* c, int mode, bool transposed, uint8_t* xq,
+                                 __nv_bfloat16* beta, cudaStream_t stream);
 size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
 fireq_status_t gemm_plan(int64_t M, int64_t N, int64_t K, int32_t* cfg);
 fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int64_t M, int64_t K,
@@ -133,7 +133,7 @@ fireq_status_t fireq_quantize_act(const void* X, int64_t M, int64_t K, int64_t l
     if (st != FIREQ_SUCCESS) return st;
     FIREQ_REQUIRE(!chan_mul || aligned16(chan_mul), FIREQ_ERROR_MISALIGNED, "fireq_quantize_act: chan_mul must be 16-byte aligned");
     return quantize_act_impl(static_cast<const __nv_bfloat16*>(X), nullptr, M, K, ldx,
-                             static_cast<const __nv_bfloat16*>(chan_mul), chan_mul ? 1 : 0, x_fp8,
+                             static_cast<const __nv_bfloat16*>(chan_mul), chan_mul ? 1 : 0, false, x_fp8,
                              static_cast<__nv_bfloat16*>(x_scale), static_cast<cudaStream_t>(stream));
 }
 
@@ -143,7 +143,38 @@ fireq_status_t fireq_silu_mul_quantize_act(const void* G, const void* U, int64_t
     if (st != FIREQ_SUCCESS) return st;
     FIREQ_REQUIRE(U && aligned16(U), FIREQ_ERROR_MISALIGNED, "fireq_silu_mul_quantize_act: U must be 16-byte aligned");
     return quantize_act_impl(static_cast<const __nv_bfloat16*>(G), static_cast<const __nv_bfloat16*>(U), M, K, ld,
-                             nullptr, 2, x_fp8, static_cast<__nv_bfloat16*>(x_scale),
+                             nullptr, 2, false, x_fp8, static_cast<__nv_bfloat16*>(x_scale),
+                             static_cast<cudaStream_t>(stream));
+}
+
+static fireq_status_t check_act_t_args(const void* Xt, int64_t M, int64_t K, int64_t ldt, uint8_t* x_fp8,
+                                       void* x_scale, const char* who) {
+    FIREQ_REQUIRE(Xt && x_fp8 && x_scale, FIREQ_ERROR_INVALID_VALUE, std::string(who) + ": NULL required pointer");
+    FIREQ_REQUIRE(M >= 1, FIREQ_ERROR_INVALID_VALUE, std::string(who) + ": M must be >= 1");
+    FIREQ_REQUIRE(K >= 128 && K % 128 == 0 && K <= 65536, FIREQ_ERROR_UNSUPPORTED_SHAPE,
+                  std::string(who) + ": K must be a multiple of 128 in [128, 65536]");
+    FIREQ_REQUIRE(ldt >= M && aligned16(x_fp8), FIREQ_ERROR_MISALIGNED,
+                  std::string(who) + ": ldt >= M and 16-byte aligned x_fp8 required");
+    return FIREQ_SUCCESS;
+}
+
+fireq_status_t fireq_quantize_act_t(const void* Xt, int64_t M, int64_t K, int64_t ldt, const void* chan_mul,
+                                    uint8_t* x_fp8, void* x_scale, void* stream) {
+    fireq_status_t st = check_act_t_args(Xt, M, K, ldt, x_fp8, x_scale, "fireq_quantize_act_t");
+    if (st != FIREQ_SUCCESS) return st;
+    FIREQ_REQUIRE(!chan_mul || aligned16(chan_mul), FIREQ_ERROR_MISALIGNED, "fireq_quantize_act_t: chan_mul must be 16-byte aligned");
+    return quantize_act_impl(static_cast<const __nv_bfloat16*>(Xt), nullptr, M, K, ldt,
+                             static_cast<const __nv_bfloat16*>(chan_mul), chan_mul ? 1 : 0, true, x_fp8,
+                             static_cast<__nv_bfloat16*>(x_scale), static_cast<cudaStream_t>(stream));
+}
+
+fireq_status_t fireq_silu_mul_quantize_act_t(const void* Gt, const void* Ut, int64_t M, int64_t K, int64_t ldt,
+                                             uint8_t* x_fp8, void* x_scale, void* stream) {
+    fireq_status_t st = check_act_t_args(Gt, M, K, ldt, x_fp8, x_scale, "fireq_silu_mul_quantize_act_t");
+    if (st != FIREQ_SUCCESS) return st;
+    FIREQ_REQUIRE(Ut, FIREQ_ERROR_INVALID_VALUE, "fireq_silu_mul_quantize_act_t: NULL Ut");
+    return quantize_act_impl(static_cast<const __nv_bfloat16*>(Gt), static_cast<const __nv_bfloat16*>(Ut), M, K, ldt,
+                             nullptr, 2, true, x_fp8, static_cast<__nv_bfloat16*>(x_scale),
                              static_cast<cudaStream_t>(stream));
 }
 
@@ -269,14 +300,14 @@ fireq_status_t fireq_comm_destroy(fireq_comm_t comm) {
 
 fireq_status_t fireq_w4a8_gemm_colpar(const uint8_t* x_fp8, const void* x_scale, int64_t M, int64_t K,
                                       const uint8_t* w_packed_local, const uint8_t* w_scales_local, int64_t N_local,
-                                      int32_t pts_exponent, void* Yt_full, void* workspace, size_t workspace_bytes,
-                                      fireq_comm_t comm, void* stream) {
+                                      int32_t pts_exponent, const float* out_chan_scale_local, void* Yt_full,
+                                      void* workspace, size_t workspace_bytes, fireq_comm_t comm, void* stream) {
     FIREQ_REQUIRE(comm && comm->comm, FIREQ_ERROR_NOT_INITIALIZED, "fireq_w4a8_gemm_colpar: comm not initialized");
     FIREQ_REQUIRE(M % 8 == 0, FIREQ_ERROR_MISALIGNED, "fireq_w4a8_gemm_colpar: M must be a multiple of 8 (Y^T rows)");
     // Y^T: rank r's slice [r*N_local, (r+1)*N_local) x M is contiguous: write it in place.
     __nv_bfloat16* slot = static_cast<__nv_bfloat16*>(Yt_full) + (size_t)comm->rank * N_local * M;
     fireq_status_t st = fireq_w4a8_gemm(x_fp8, x_scale, M, K, w_packed_local, w_scales_local, N_local, pts_exponent,
-                                        nullptr, slot, M, 1, workspace, workspace_bytes, stream);
+                                        out_chan_scale_local, slot, M, 1, workspace, workspace_bytes, stream);
     if (st != FIREQ_SUCCESS) return st;
     if (comm->nranks == 1) return FIREQ_SUCCESS;
     const int r = nccl().allgather(slot, Yt_full, (size_t)N_local * M, /*ncclBfloat16=*/9, comm->comm,

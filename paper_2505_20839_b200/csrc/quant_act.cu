@@ -34,10 +34,23 @@ struct Src {
     const __nv_bfloat16* U;   // silu-mul mode: X = gate, U = up
     const __nv_bfloat16* c;
     int mode;                 // 0 = plain, 1 = channel multiplier, 2 = silu(g) * u
+    int transposed;           // element (m, k) at X[k * ld + m] (Y^T of the column-parallel GEMM)
+    int64_t ld;
 };
 
-__device__ __forceinline__ void load8(const Src& s, int64_t row_off, int64_t k, float (&v)[8]) {
-    const uint4 rx = *reinterpret_cast<const uint4*>(s.X + row_off + k);
+// 8 consecutive k of row m; row-major rows are loaded as one 16-B vector, transposed
+// inputs element by element (decode-sized M only).
+__device__ __forceinline__ uint4 load8_raw(const __nv_bfloat16* base, const Src& s, int64_t m, int64_t k) {
+    if (!s.transposed) return *reinterpret_cast<const uint4*>(base + m * s.ld + k);
+    uint4 r;
+    __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(&r);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) h[i] = base[(k + i) * s.ld + m];
+    return r;
+}
+
+__device__ __forceinline__ void load8(const Src& s, int64_t m, int64_t k, float (&v)[8]) {
+    const uint4 rx = load8_raw(s.X, s, m, k);
     const __nv_bfloat16* hx = reinterpret_cast<const __nv_bfloat16*>(&rx);
     if (s.mode == 0) {
 #pragma unroll
@@ -49,7 +62,7 @@ __device__ __forceinline__ void load8(const Src& s, int64_t row_off, int64_t k, 
         for (int i = 0; i < 8; ++i)
             v[i] = __bfloat162float(__float2bfloat16_rn(__fmul_rn(__bfloat162float(hx[i]), __bfloat162float(hc[i]))));
     } else {
-        const uint4 ru = *reinterpret_cast<const uint4*>(s.U + row_off + k);
+        const uint4 ru = load8_raw(s.U, s, m, k);
         const __nv_bfloat16* hu = reinterpret_cast<const __nv_bfloat16*>(&ru);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -64,7 +77,7 @@ __device__ __forceinline__ void load8(const Src& s, int64_t row_off, int64_t k, 
 // [rank*K/CL, (rank+1)*K/CL) of token row m; the row amax is combined across the
 // cluster through distributed shared memory (DSMEM).  CL = 8 for decode-sized M
 // (spreads a 16-token batch over 128 CTAs), 1 for large M.
-__global__ void __launch_bounds__(kThreads) k_act_quant(Src s, int64_t M, int64_t K, int64_t ld, int cl,
+__global__ void __launch_bounds__(kThreads) k_act_quant(Src s, int64_t M, int64_t K, int cl,
                                                         uint8_t* __restrict__ xq,
                                                         __nv_bfloat16* __restrict__ beta_out) {
     __shared__ float red[32];
@@ -72,13 +85,12 @@ __global__ void __launch_bounds__(kThreads) k_act_quant(Src s, int64_t M, int64_
     ptx::pdl_wait();                       // X / G / U come from the previous kernel
     const int rank = cl > 1 ? (int)ptx::cluster_ctarank() : 0;
     for (int64_t m = blockIdx.y; m < M; m += gridDim.y) {
-    const int64_t row_off = m * ld;
     const int64_t chunk = K / cl;
     const int64_t k0 = rank * chunk, k1 = k0 + chunk;
     float amax = 0.0f;
     for (int64_t k = k0 + (int64_t)threadIdx.x * 8; k < k1; k += kThreads * 8) {
         float v[8];
-        load8(s, row_off, k, v);
+        load8(s, m, k, v);
 #pragma unroll
         for (int i = 0; i < 8; ++i) amax = fmaxf(amax, fabsf(v[i]));
     }
@@ -103,7 +115,7 @@ __global__ void __launch_bounds__(kThreads) k_act_quant(Src s, int64_t M, int64_
     // A3: x_hat = E4M3_RN_satfinite(x' / beta)
     for (int64_t k = k0 + (int64_t)threadIdx.x * 8; k < k1; k += kThreads * 8) {
         float v[8];
-        load8(s, row_off, k, v);
+        load8(s, m, k, v);
         uint2 o;
         o.x = e4m3x2_rn(__fdiv_rn(v[0], beta), __fdiv_rn(v[1], beta)) |
               (e4m3x2_rn(__fdiv_rn(v[2], beta), __fdiv_rn(v[3], beta)) << 16);
@@ -118,13 +130,13 @@ __global__ void __launch_bounds__(kThreads) k_act_quant(Src s, int64_t M, int64_
 }  // namespace
 
 fireq_status_t quantize_act_impl(const __nv_bfloat16* X, const __nv_bfloat16* U, int64_t M, int64_t K,
-                                 int64_t ld, const __nv_bfloat16* c, int mode, uint8_t* xq,
+                                 int64_t ld, const __nv_bfloat16* c, int mode, bool transposed, uint8_t* xq,
                                  __nv_bfloat16* beta, cudaStream_t stream) {
-    Src s{X, U, c, mode};
+    Src s{X, U, c, mode, transposed ? 1 : 0, ld};
     const int cl = M <= 64 ? 8 : 1;
     const unsigned rows = (unsigned)std::min<int64_t>(M, 65535);
     const cudaError_t e = launch_ex(k_act_quant, dim3((unsigned)cl, rows), dim3(kThreads), 0, stream,
-                                    (unsigned)cl, s, M, K, ld, cl, xq, beta);
+                                    (unsigned)cl, s, M, K, cl, xq, beta);
     if (e != cudaSuccess) return fail(FIREQ_ERROR_CUDA, std::string("act quant launch: ") + cudaGetErrorString(e));
     return check_launch(mode == 2 ? "fireq_silu_mul_quantize_act" : "fireq_quantize_act");
 }

@@ -22,6 +22,7 @@ EXPORTS = [
     "fireq_quantize_weight", "fireq_quantize_act", "fireq_silu_mul_quantize_act",
     "fireq_w4a8_gemm", "fireq_comm_get_unique_id", "fireq_comm_init", "fireq_comm_destroy",
     "fireq_w4a8_gemm_colpar", "fireq_debug_lut_table", "fireq_gemm_plan", "fireq_debug_set_trace",
+    "fireq_quantize_act_t", "fireq_silu_mul_quantize_act_t",
 ]
 
 
@@ -53,7 +54,9 @@ def load(path=LIB_PATH):
         "fireq_comm_get_unique_id": ([P], C),
         "fireq_comm_init": ([P, C, C, P], C),
         "fireq_comm_destroy": ([P], C),
-        "fireq_w4a8_gemm_colpar": ([P, P, I64, I64, P, P, I64, I32, P, P, SZ, P, P], C),
+        "fireq_w4a8_gemm_colpar": ([P, P, I64, I64, P, P, I64, I32, P, P, P, SZ, P, P], C),
+        "fireq_quantize_act_t": ([P, I64, I64, I64, P, P, P, P], C),
+        "fireq_silu_mul_quantize_act_t": ([P, P, I64, I64, I64, P, P, P], C),
         "fireq_debug_lut_table": ([P, P], C),
         "fireq_gemm_plan": ([I64, I64, I64, P], C),
         "fireq_debug_set_trace": ([P], C),
@@ -180,6 +183,32 @@ def silu_mul_quantize_act(G, U, stream=None, out=None):
     return xq, beta
 
 
+def quantize_act_t(Xt, M, K, chan_mul=None, stream=None, out=None):
+    """Transposed input Xt [K][ldt] (element (m, k) at Xt[k, m]) -> (x_fp8 [M][K], beta [M])."""
+    assert Xt.dtype == torch.bfloat16 and Xt.stride(1) == 1
+    if out is None:
+        xq = torch.empty((M, K), dtype=torch.uint8, device=Xt.device)
+        beta = torch.empty(M, dtype=torch.bfloat16, device=Xt.device)
+    else:
+        xq, beta = out
+    _check(lib().fireq_quantize_act_t(_ptr(Xt), M, K, Xt.stride(0), _ptr(chan_mul), _ptr(xq), _ptr(beta),
+                                      _stream(stream)), "fireq_quantize_act_t")
+    return xq, beta
+
+
+def silu_mul_quantize_act_t(Gt, Ut, M, K, stream=None, out=None):
+    """Gt, Ut [K][ldt] (Y^T layout) -> quantized silu(g) * u as (x_fp8 [M][K], beta [M])."""
+    assert Gt.stride() == Ut.stride() and Gt.stride(1) == 1
+    if out is None:
+        xq = torch.empty((M, K), dtype=torch.uint8, device=Gt.device)
+        beta = torch.empty(M, dtype=torch.bfloat16, device=Gt.device)
+    else:
+        xq, beta = out
+    _check(lib().fireq_silu_mul_quantize_act_t(_ptr(Gt), _ptr(Ut), M, K, Gt.stride(0), _ptr(xq), _ptr(beta),
+                                               _stream(stream)), "fireq_silu_mul_quantize_act_t")
+    return xq, beta
+
+
 class Workspace:
     """Zero-initialised GEMM workspace (the counters must start at zero, fireq.h)."""
 
@@ -241,10 +270,13 @@ class Comm:
             self.h = ctypes.c_void_p()
 
 
-def w4a8_gemm_colpar(xq, beta, packed_local, scales_local, N_local, pts_n, comm, Yt_full, workspace, stream=None):
+def w4a8_gemm_colpar(xq, beta, packed_local, scales_local, N_local, pts_n, comm, Yt_full, workspace,
+                     gamma_local=None, stream=None):
+    """Column-parallel GEMM: this rank's Y^T slice + in-place NCCL all-gather into Yt_full [P*N_local][M]."""
     M, K = xq.shape
     ws = workspace.ensure(lib().fireq_w4a8_gemm_workspace_bytes(M, N_local, K))
     _check(lib().fireq_w4a8_gemm_colpar(_ptr(xq), _ptr(beta), M, K, _ptr(packed_local), _ptr(scales_local), N_local,
-                                        pts_n, _ptr(Yt_full), _ptr(ws), ws.numel(), comm.h, _stream(stream)),
+                                        pts_n, _ptr(gamma_local), _ptr(Yt_full), _ptr(ws), ws.numel(), comm.h,
+                                        _stream(stream)),
            "fireq_w4a8_gemm_colpar")
     return Yt_full

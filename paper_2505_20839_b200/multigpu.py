@@ -1,0 +1,124 @@
+"""Column-parallel FFN across the GPUs of one node (bench.py --gpus N, launched by torchrun).
+
+One process per GPU.  Every rank quantizes the full FFN weights with
+fireq_quantize_weight (deterministic, so CAS lambda and PTS n are identical on all
+ranks) and keeps its N-shard (sharding.py).  A decode step on rank r:
+
+  fireq_quantize_act(x, c_gu)                         replicated (bit-identical on all ranks)
+  fireq_w4a8_gemm_colpar(W_gu shard r)  -> GU^T       rank's slice + in-place NCCL all-gather
+  fireq_silu_mul_quantize_act_t(GU^T)                 replicated
+  fireq_w4a8_gemm_colpar(W_down shard r) -> Y^T       slice + in-place NCCL all-gather
+
+The only data-path collectives are the two output all-gathers (north_star (d)); the
+communicator is libfireq's own NCCL communicator (unique id broadcast by torch.distributed,
+which is used for plumbing only: barriers and the max-over-ranks timing).
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import sharding
+
+D_MODEL, D_FF = 4096, 11008
+
+
+def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src):
+    import synth
+    M = 16
+    R = 4
+    uid = F.Comm.unique_id() if rank == 0 else None
+    box = [uid]
+    dist.broadcast_object_list(box, src=0)
+    comm = F.Comm(world, rank, box[0])
+
+    wg = synth.weights(D_FF, D_MODEL, synth.layer_seed(1, 0))
+    wu = synth.weights(D_FF, D_MODEL, synth.layer_seed(1, 1))
+    wd = synth.weights(D_MODEL, D_FF, synth.layer_seed(1, 2))
+    W_gu = synth.bits_to_torch(np.concatenate([wg, wu], axis=0)).to(dev)
+    W_d = synth.bits_to_torch(wd).to(dev)
+    q_gu = F.quantize_weight(W_gu, cas_mode=1)
+    q_d = F.quantize_weight(W_d, cas_mode=1)
+    n_gu, n_d = q_gu.n, q_d.n
+    del W_gu, W_d
+    plan_gu = sharding.ShardPlan(2 * D_FF, world)
+    plan_d = sharding.ShardPlan(D_MODEL, world)
+    zeros_u8 = lambda n: torch.zeros(n, dtype=torch.uint8, device=dev)
+    gamma_full = torch.cat([torch.ones(D_FF, device=dev), q_d.c.float()])
+    gamma_l = sharding.shard_vector(gamma_full, plan_gu, rank, lambda n: torch.ones(n, device=dev))
+    rot = []
+    for _ in range(R):
+        pg, sg = sharding.shard_quantized(q_gu.packed, q_gu.scales, plan_gu, rank, D_MODEL, zeros_u8)
+        pd, sd = sharding.shard_quantized(q_d.packed, q_d.scales, plan_d, rank, D_FF, zeros_u8)
+        rot.append((pg, sg, pd, sd))
+    x = synth.bits_to_torch(synth.activations(M, D_MODEL, synth.layer_seed(1, 3))).to(dev)
+    xq = torch.empty((M, D_MODEL), dtype=torch.uint8, device=dev)
+    beta = torch.empty(M, dtype=torch.bfloat16, device=dev)
+    gut = torch.empty((plan_gu.N_pad, M), dtype=torch.bfloat16, device=dev)
+    hq = torch.empty((M, D_FF), dtype=torch.uint8, device=dev)
+    hbeta = torch.empty(M, dtype=torch.bfloat16, device=dev)
+    yt = torch.empty((plan_d.N_pad, M), dtype=torch.bfloat16, device=dev)
+    ws1 = F.Workspace(F.gemm_workspace_bytes(M, plan_gu.N_local, D_MODEL), dev)
+    ws2 = F.Workspace(F.gemm_workspace_bytes(M, plan_d.N_local, D_FF), dev)
+
+    def step(r):
+        pg, sg, pd, sd = rot[r]
+        F.quantize_act(x, chan_mul=q_gu.c, out=(xq, beta), stream=stream)
+        F.w4a8_gemm_colpar(xq, beta, pg, sg, plan_gu.N_local, n_gu, comm, gut, ws1, gamma_local=gamma_l,
+                           stream=stream)
+        F.silu_mul_quantize_act_t(gut[:D_FF], gut[D_FF:2 * D_FF], M, D_FF, out=(hq, hbeta), stream=stream)
+        F.w4a8_gemm_colpar(hq, hbeta, pd, sd, plan_d.N_local, n_d, comm, yt, ws2, stream=stream)
+
+    with torch.cuda.stream(stream):
+        for r in range(R):
+            step(r)
+    torch.cuda.synchronize()
+    graphed = True
+    try:
+        g_multi = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_multi, stream=stream):
+            for r in range(R):
+                step(r)
+        replay = lambda: g_multi.replay()
+        per_call = R
+    except Exception as e:                      # NCCL capture unsupported: eager launches
+        graphed = False
+        print(f"[rank {rank}] graph capture failed ({e}); timing eager launches", file=sys.stderr)
+        replay = lambda: [step(r) for r in range(R)]
+        per_call = R
+    calls = max(1, args.steps // per_call)
+    steps = calls * per_call
+    for _ in range(max(1, args.warmup // per_call)):
+        with torch.cuda.stream(stream):
+            replay()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(calls):
+            replay()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    us_per_step = float(ms.item()) * 1e3 / steps
+    comm.destroy()
+    if rank == 0:
+        line = {
+            "metric": "Llama2-7B FFN latency at batch 16 (W4A8-FP: INT4 weights + FP8 g128 scales, FP8 activations)",
+            "value": round(us_per_step, 3), "unit": "us", "n_gpus": world, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": round(us_per_step / 1e3, 6), "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "fp8e4m3 x int4 -> f32 acc -> bf16", "data": "synthetic",
+            "config": {"workload": "llama2-7b-ffn-decode-b16", "tokens": M, "d_model": D_MODEL, "d_ff": D_FF,
+                       "parallelism": f"column-parallel tp{world} (N-sharded gate_up + down, NCCL all-gather of Y^T)",
+                       "l2": f"{R} rotating weight-shard copies", "graph": "captured" if graphed else "eager"},
+            "gpu_launches": 4 * steps,
+        }
+        print(json.dumps(line), flush=True)

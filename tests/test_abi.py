@@ -1,0 +1,64 @@
+"""The C-ABI library loads on CPU and exports every function include/fireq.h declares.
+
+No compute calls (no GPU here): only pure host entry points (sizes, status strings)
+and argument validation paths that return before touching CUDA.
+"""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2505_20839_b200 import fireq as F
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "fireq.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(fireq_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(F.LIB_PATH):
+        import __graft_entry__
+        __graft_entry__.build()
+    return F.load()
+
+
+def test_exports_every_declared_symbol(lib):
+    names = declared_functions()
+    assert len(names) >= 15
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(F.EXPORTS) <= set(names)
+
+
+def test_host_only_entry_points(lib):
+    assert lib.fireq_weight_layout_version() == 1
+    assert lib.fireq_packed_weight_bytes(4096, 4096) == 4096 * 4096 // 2
+    assert lib.fireq_weight_scale_bytes(4096, 4096) == 4096 * 4096 // 128
+    assert lib.fireq_quantize_weight_workspace_bytes(128, 4096) >= 4096 * 8
+    assert lib.fireq_status_string(0) == b"FIREQ_SUCCESS"
+    assert lib.fireq_status_string(3) == b"FIREQ_ERROR_MISALIGNED"
+
+
+def test_argument_validation_without_gpu(lib):
+    P = ctypes.c_void_p
+    # NULL pointers -> INVALID_VALUE before any CUDA call
+    st = lib.fireq_w4a8_gemm(None, None, 16, 4096, None, None, 4096, 0, None, None, 4096, 0, None, 0, None)
+    assert st == 1 and b"NULL" in lib.fireq_last_error()
+    # bad shape -> UNSUPPORTED_SHAPE; misaligned -> MISALIGNED
+    buf = ctypes.create_string_buffer(1 << 12)
+    base = ctypes.addressof(buf)
+    a16 = P((base + 15) & ~15)
+    st = lib.fireq_w4a8_gemm(a16, a16, 16, 4000, a16, a16, 4096, 0, None, a16, 4096, 0, a16, 1, None)
+    assert st == 2
+    st = lib.fireq_w4a8_gemm(P(a16.value + 1), a16, 16, 4096, a16, a16, 4096, 0, None, a16, 4096, 0, a16, 1, None)
+    assert st == 3
+    st = lib.fireq_quantize_weight(a16, 128, 128, 7, a16, a16, None, None, a16, a16, 1 << 20, None)
+    assert st == 1                                    # cas_mode 7
+    st = lib.fireq_quantize_act(a16, 0, 128, 128, None, a16, a16, None)
+    assert st == 1                                    # M = 0
