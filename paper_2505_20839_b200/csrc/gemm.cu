@@ -205,7 +205,8 @@ struct Cfg {
     static constexpr int kOffS = kOffW + STAGES * kWStage;
     static constexpr int kOffLut = kOffS + STAGES * kSStage;
     static constexpr int kOffFix = kOffLut + 2048;
-    static constexpr int kOffBar = kOffFix + kFixSlots * kPartBytes;
+    static constexpr int kOffEpi = kOffFix + kFixSlots * kPartBytes;    // scales [NTOK] + 4 KB transpose
+    static constexpr int kOffBar = kOffEpi + 1024 + 16 * kTileN * 2;
     static constexpr int kNumBars = 3 * STAGES + 2 * ASTAGES + 2 * ACCBUF + 1;
     static constexpr int kOffMisc = kOffBar + kNumBars * 8;
     static constexpr int kSmemBytes = kOffMisc + 64 + 1024;             // + alignment slack
@@ -330,11 +331,11 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
         ptx::tmem_alloc(&misc[0], C::kTmemCols);
         ptx::tmem_relinquish();
     }
-    if (warp == kWAlloc || warp == kWProdX) {
+    {
         // LUT-of-LUTs: entry [s][u] = E4M3_RN(v(u) * sigma_s) for all 127 finite sigma codes
-        // (Step 1's 16-entry table).  v * sigma is exact in fp32.
+        // (Step 1's 16-entry table).  v * sigma is exact in fp32.  All threads.
         uint8_t* lut = reinterpret_cast<uint8_t*>(sLut);
-        for (int e = threadIdx.x - kWAlloc * 32; e < kLutEntries; e += 64) {
+        for (int e = threadIdx.x; e < kLutEntries; e += C::kThreads) {
             const int s = e >> 4, u = e & 15;
             const float v = (float)(u < 8 ? u : u - 16);
             lut[e] = (uint8_t)e4m3_rn(__fmul_rn(v, e4m3_decode((uint32_t)s)));
@@ -357,7 +358,9 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
         // Weights never depend on the previous kernel, so this warp streams them from
         // the start (PDL overlap); the whole warp walks the schedule and one elected
         // lane issues (a lane-0 branch makes the compiler wrap TMAs in waterfall loops).
-        const uint64_t pol_w = ptx::policy_evict_first();   // weights: streamed once
+        // decode: weights are streamed once (evict first); prefill: every m-tile re-reads
+        // them, so keep them in L2 (the 126 MB L2 holds the largest layer's weights)
+        const uint64_t pol_w = a.m_tiles == 1 ? ptx::policy_evict_first() : ptx::policy_evict_last();
         st.init(a, blockIdx.x);
         int i = 0;
         while (st.next(nt, mt, g, ng, sfirst, slast)) {
@@ -379,7 +382,9 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
         }
     } else if (warp == kWProdX) {
         // ------------------------------------------------------- activation producer
-        const uint64_t pol_x = ptx::policy_evict_last();    // activations: re-read by every tile
+        // decode: the activation tile is re-read by every n-tile; prefill: the concurrent CTAs
+        // share one m-tile, then it is dead
+        const uint64_t pol_x = a.m_tiles == 1 ? ptx::policy_evict_last() : ptx::policy_evict_first();
         ptx::pdl_wait();                    // activations are written by the previous kernel
         st.init(a, blockIdx.x);
         int i = 0;
@@ -553,10 +558,49 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
         const int r = threadIdx.x & 127;
         const uint32_t lane_base = (uint32_t)(r & ~31) << 16;
         const float p2 = exp2_neg(a.pts_n);
+        float* sScale = reinterpret_cast<float*>(smem + C::kOffEpi);                 // [NTOK]
+        __nv_bfloat16* sT = reinterpret_cast<__nv_bfloat16*>(smem + C::kOffEpi + 1024);  // [16][128]
         it.init(a, blockIdx.x);
         int sg = 0, i_stage = 0;
         uint32_t fix_phase = 0;
         const long long u_first = (long long)blockIdx.x * a.U / a.C;
+        int ntile = 0, m0 = 0, n = 0;
+        float gam = 1.0f;
+        // Step 3 for 16 tokens [m0 + 16 ch, +16) of this thread's output channel n:
+        // y = bf16(acc * (beta_m 2^-n) [* gamma_n]).  Y^T rows are 32 contiguous bytes per
+        // thread; row-major Y goes through a 4 KB SMEM transpose so that each warp writes
+        // whole 256-byte rows with 16-byte stores.
+        auto emit = [&](const float (&acc)[16], int ch) {
+            __align__(16) __nv_bfloat16 yb[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                float y = __fmul_rn(acc[c], sScale[ch * 16 + c]);
+                if (a.gamma) y = __fmul_rn(y, gam);
+                yb[c] = __float2bfloat16_rn(y);
+            }
+            const int mb = m0 + ch * 16;
+            if (a.out_layout == 1) {
+                __nv_bfloat16* dst = a.Y + (size_t)n * a.ldy + mb;
+                if (mb + 16 <= a.M) {
+                    reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<const uint4*>(yb)[0];
+                    reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<const uint4*>(yb)[1];
+                } else {
+                    for (int c = 0; c < 16 && mb + c < a.M; ++c) dst[c] = yb[c];
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < 16; ++c) sT[c * kTileN + r] = yb[c];
+                ptx::named_bar_sync(1, 128);
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const int piece = r + 128 * k, row = piece >> 4, seg = piece & 15;
+                    if (mb + row < a.M)
+                        *reinterpret_cast<uint4*>(a.Y + (size_t)(mb + row) * a.ldy + ntile * kTileN + seg * 8) =
+                            *reinterpret_cast<const uint4*>(sT + row * kTileN + seg * 8);
+                }
+                ptx::named_bar_sync(1, 128);
+            }
+        };
         while (it.next(tile, g0, g1)) {
             const int b = sg % ACCBUF;
             // with NMMA issuers, accumulator w holds the stages i of this segment with
@@ -565,16 +609,20 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
             const int w_first = i_stage % NMMA;
             const bool both = NMMA == 2 && nstages >= 2;
             i_stage += nstages;
-            ptx::mbar_wait(&accfull[b], (sg / ACCBUF) & 1);
-            ptx::tc_fence_after();
-            const int ntile = tile % a.n_tiles, mtile = tile / a.n_tiles;
-            const int n = ntile * kTileN + r;
-            const int m0 = mtile * NTOK;
+            ntile = tile % a.n_tiles;
+            const int mtile = tile / a.n_tiles;
+            n = ntile * kTileN + r;
+            m0 = mtile * NTOK;
+            gam = a.gamma ? a.gamma[n] : 1.0f;
+            for (int t = r; t < NTOK; t += 128)
+                sScale[t] = (m0 + t < a.M) ? __fmul_rn(__bfloat162float(a.x_scale[m0 + t]), p2) : 0.0f;
             const bool whole = (g0 == 0 && g1 == a.G);
             int slot = 0;
             if (!whole) slot = 2 * blockIdx.x + ((u_first < (long long)tile * a.G) ? 1 : 0);   // first/last segment
-            const float gam = a.gamma ? a.gamma[n] : 1.0f;
             float* part = a.partial + (size_t)slot * NTOK * kTileN;
+            ptx::mbar_wait(&accfull[b], (sg / ACCBUF) & 1);
+            ptx::tc_fence_after();
+            ptx::named_bar_sync(1, 128);            // sScale visible
 #pragma unroll 1
             for (int ch = 0; ch < NTOK / 16; ++ch) {
                 uint32_t v[16];
@@ -591,17 +639,10 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                     ptx::tmem_wait_ld();
                 }
                 if (whole) {
+                    float accv[16];
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) {
-                        const int m = m0 + ch * 16 + c;
-                        if (m < a.M) {
-                            float y = __fmul_rn(__uint_as_float(v[c]), __fmul_rn(__bfloat162float(a.x_scale[m]), p2));
-                            if (a.gamma) y = __fmul_rn(y, gam);
-                            const __nv_bfloat16 yb = __float2bfloat16_rn(y);
-                            if (a.out_layout == 0) a.Y[(size_t)m * a.ldy + n] = yb;
-                            else a.Y[(size_t)n * a.ldy + m] = yb;
-                        }
-                    }
+                    for (int c = 0; c < 16; ++c) accv[c] = __uint_as_float(v[c]);
+                    emit(accv, ch);
                 } else {
 #pragma unroll
                     for (int c = 0; c < 16; ++c) part[(ch * 16 + c) * kTileN + r] = __uint_as_float(v[c]);
@@ -628,7 +669,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                     // Stage the contributors' partials (contiguous kPartBytes blocks) into SMEM
                     // with bulk copies, kFixSlots per round trip, and sum them in CTA order.
                     asm volatile("fence.proxy.async.global;" ::: "memory");
-                    float accv[NTOK];
+                    float accv[C::kFixSlots > 0 ? NTOK : 1];
 #pragma unroll
                     for (int c = 0; c < NTOK; ++c) accv[c] = 0.0f;
                     for (int cc0 = c_lo; cc0 <= c_hi; cc0 += (C::kFixSlots > 0 ? C::kFixSlots : 1)) {
@@ -653,26 +694,22 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                         ptx::named_bar_sync(1, 128);      // sFix reuse
                     }
 #pragma unroll
-                    for (int c = 0; c < NTOK; ++c) {
-                        const int m = m0 + c;
-                        if (m < a.M) {
-                            float y = __fmul_rn(accv[c], __fmul_rn(__bfloat162float(a.x_scale[m]), p2));
-                            if (a.gamma) y = __fmul_rn(y, gam);
-                            const __nv_bfloat16 yb = __float2bfloat16_rn(y);
-                            if (a.out_layout == 0) a.Y[(size_t)m * a.ldy + n] = yb;
-                            else a.Y[(size_t)n * a.ldy + m] = yb;
-                        }
+                    for (int ch = 0; ch < NTOK / 16; ++ch) {
+                        float e[16];
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) e[c] = accv[ch * 16 + c];
+                        emit(e, ch);
                     }
                 } else if (misc[1]) {
                     __threadfence();
 #pragma unroll 1
-                    for (int ch = 0; ch < NTOK / 8; ++ch) {
-                        float accv[8];
+                    for (int ch = 0; ch < NTOK / 16; ++ch) {
+                        float accv[16];
 #pragma unroll
-                        for (int c = 0; c < 8; ++c) accv[c] = 0.0f;
+                        for (int c = 0; c < 16; ++c) accv[c] = 0.0f;
                         // contributors in CTA order; loads of up to 4 contributors in flight
                         for (int cc0 = c_lo; cc0 <= c_hi; cc0 += 4) {
-                            float tmp[4][8];
+                            float tmp[4][16];
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
                                 const int cc = cc0 + q;
@@ -681,28 +718,18 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                                     const int sl = 2 * cc + ((cu0 < t0) ? 1 : 0);
                                     const float* pp = a.partial + (size_t)sl * NTOK * kTileN;
 #pragma unroll
-                                    for (int c = 0; c < 8; ++c) tmp[q][c] = __ldcg(pp + (ch * 8 + c) * kTileN + r);
+                                    for (int c = 0; c < 16; ++c) tmp[q][c] = __ldcg(pp + (ch * 16 + c) * kTileN + r);
                                 }
                             }
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
                                 if (cc0 + q <= c_hi) {
 #pragma unroll
-                                    for (int c = 0; c < 8; ++c) accv[c] = __fadd_rn(accv[c], tmp[q][c]);
+                                    for (int c = 0; c < 16; ++c) accv[c] = __fadd_rn(accv[c], tmp[q][c]);
                                 }
                             }
                         }
-#pragma unroll
-                        for (int c = 0; c < 8; ++c) {
-                            const int m = m0 + ch * 8 + c;
-                            if (m < a.M) {
-                                float y = __fmul_rn(accv[c], __fmul_rn(__bfloat162float(a.x_scale[m]), p2));
-                                if (a.gamma) y = __fmul_rn(y, gam);
-                                const __nv_bfloat16 yb = __float2bfloat16_rn(y);
-                                if (a.out_layout == 0) a.Y[(size_t)m * a.ldy + n] = yb;
-                                else a.Y[(size_t)n * a.ldy + m] = yb;
-                            }
-                        }
+                        emit(accv, ch);
                     }
                 }
                 if (misc[1] && r == 0) {
@@ -781,7 +808,7 @@ struct Plan {
 
 Plan make_plan(int64_t M, int64_t N, int64_t K) {
     Plan p{};
-    p.ntok = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
+    p.ntok = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 192;
     p.sign_split = p.ntok <= 128;
     p.m_tiles = (int)((M + p.ntok - 1) / p.ntok);
     p.n_tiles = (int)(N / kTileN);
@@ -876,7 +903,7 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
         case 32:  return launch_cfg<32, true, 3, 7, 3, 2, 2, 1>(map, args, stream);
         case 64:  return launch_cfg<64, true, 2, 5, 2, 2, 2, 1>(map, args, stream);
         case 128: return launch_cfg<128, true, 2, 7, 4, 2, 1, 1>(map, args, stream);
-        default:  return launch_cfg<256, false, 2, 4, 4, 1, 1, 1>(map, args, stream);
+        default:  return launch_cfg<192, false, 2, 6, 4, 2, 1, 1>(map, args, stream);
     }
 }
 
