@@ -20,7 +20,7 @@ __device__ __forceinline__ float block_max(float v, float* red) {
     if (l == 0) red[w] = v;
     __syncthreads();
     if (w == 0) {
-        v = l < (kThreads / 32) ? red[l] : 0.0f;
+        v = l < (int)(blockDim.x >> 5) ? red[l] : 0.0f;
         for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
         if (l == 0) red[0] = v;
     }
@@ -49,82 +49,106 @@ __device__ __forceinline__ uint4 load8_raw(const __nv_bfloat16* base, const Src&
     return r;
 }
 
-__device__ __forceinline__ void load8(const Src& s, int64_t m, int64_t k, float (&v)[8]) {
+// x' (bf16 values, A1 / SiLU*mul) of 8 consecutive elements, packed as 8 bf16.
+__device__ __forceinline__ uint4 xprime8(const Src& s, int64_t m, int64_t k) {
     const uint4 rx = load8_raw(s.X, s, m, k);
+    if (s.mode == 0) return rx;
     const __nv_bfloat16* hx = reinterpret_cast<const __nv_bfloat16*>(&rx);
-    if (s.mode == 0) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = __bfloat162float(hx[i]);
-    } else if (s.mode == 1) {
+    uint4 out;
+    __nv_bfloat16* ho = reinterpret_cast<__nv_bfloat16*>(&out);
+    if (s.mode == 1) {
         const uint4 rc = *reinterpret_cast<const uint4*>(s.c + k);
         const __nv_bfloat16* hc = reinterpret_cast<const __nv_bfloat16*>(&rc);
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-            v[i] = __bfloat162float(__float2bfloat16_rn(__fmul_rn(__bfloat162float(hx[i]), __bfloat162float(hc[i]))));
+            ho[i] = __float2bfloat16_rn(__fmul_rn(__bfloat162float(hx[i]), __bfloat162float(hc[i])));
     } else {
         const uint4 ru = load8_raw(s.U, s, m, k);
         const __nv_bfloat16* hu = reinterpret_cast<const __nv_bfloat16*>(&ru);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const float g = __bfloat162float(hx[i]);
-            const float silu = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
-            v[i] = __bfloat162float(__float2bfloat16_rn(__fmul_rn(silu, __bfloat162float(hu[i]))));
+            const float silu = __fdividef(g, 1.0f + __expf(-g));     // SiLU: tolerance-checked (DESIGN R17)
+            ho[i] = __float2bfloat16_rn(__fmul_rn(silu, __bfloat162float(hu[i])));
         }
     }
+    return out;
 }
 
-// Grid (CL, M), cluster (CL, 1, 1): CTA `rank` of a cluster quantizes columns
+// Grid (CL, rows), cluster (CL, 1, 1): CTA `rank` of a cluster quantizes columns
 // [rank*K/CL, (rank+1)*K/CL) of token row m; the row amax is combined across the
 // cluster through distributed shared memory (DSMEM).  CL = 8 for decode-sized M
-// (spreads a 16-token batch over 128 CTAs), 1 for large M.
-__global__ void __launch_bounds__(kThreads) k_act_quant(Src s, int64_t M, int64_t K, int cl,
-                                                        uint8_t* __restrict__ xq,
-                                                        __nv_bfloat16* __restrict__ beta_out) {
+// (spreads a 16-token batch over 128 CTAs), 1 for large M.  Each thread keeps its
+// (at most R) 8-element vectors of x' in registers between the amax and encode passes.
+template <int R>
+__global__ void __launch_bounds__(1024) k_act_quant(Src s, int64_t M, int64_t K, int cl,
+                                                   uint8_t* __restrict__ xq,
+                                                   __nv_bfloat16* __restrict__ beta_out) {
     __shared__ float red[32];
     ptx::pdl_trigger();
     ptx::pdl_wait();                       // X / G / U come from the previous kernel
     const int rank = cl > 1 ? (int)ptx::cluster_ctarank() : 0;
-    for (int64_t m = blockIdx.y; m < M; m += gridDim.y) {
     const int64_t chunk = K / cl;
     const int64_t k0 = rank * chunk, k1 = k0 + chunk;
-    float amax = 0.0f;
-    for (int64_t k = k0 + (int64_t)threadIdx.x * 8; k < k1; k += kThreads * 8) {
-        float v[8];
-        load8(s, m, k, v);
+    const int nt = blockDim.x;
+    for (int64_t m = blockIdx.y; m < M; m += gridDim.y) {
+        uint4 xv[R];
+        float amax = 0.0f;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) amax = fmaxf(amax, fabsf(v[i]));
-    }
-    amax = block_max(amax, red);           // red[0] = this CTA's max
-    if (cl > 1) {
-        ptx::cluster_sync();               // every CTA's red[0] is written
-        if (threadIdx.x < 32) {
-            float v = 0.0f;
-            if (threadIdx.x < (unsigned)cl)
-                v = ptx::ld_shared_cluster_f32(ptx::mapa_shared(ptx::smem_u32(&red[0]), threadIdx.x));
-            for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-            if (threadIdx.x == 0) red[1] = v;
+        for (int j = 0; j < R; ++j) {
+            const int64_t k = k0 + ((int64_t)j * nt + threadIdx.x) * 8;
+            if (k < k1) {
+                xv[j] = xprime8(s, m, k);
+                const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&xv[j]);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) amax = fmaxf(amax, fabsf(__bfloat162float(h[i])));
+            }
         }
-        ptx::cluster_sync();               // remote reads done before any CTA moves on / exits
-        amax = red[1];
+        amax = block_max(amax, red);           // red[0] = this CTA's max
+        if (cl > 1) {
+            ptx::cluster_sync();               // every CTA's red[0] is written
+            if (threadIdx.x < 32) {
+                float v = 0.0f;
+                if (threadIdx.x < (unsigned)cl)
+                    v = ptx::ld_shared_cluster_f32(ptx::mapa_shared(ptx::smem_u32(&red[0]), threadIdx.x));
+                for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+                if (threadIdx.x == 0) red[1] = v;
+            }
+            ptx::cluster_sync();               // remote reads done before any CTA moves on / exits
+            amax = red[1];
+        }
+        // A2: beta = bf16_RN(amax / 448) (fp32 division then RNE; equals exact RNE for bf16 operands)
+        const __nv_bfloat16 beta_h = amax > 0.0f ? __float2bfloat16_rn(__fdiv_rn(amax, 448.0f))
+                                                 : __float2bfloat16_rn(1.0f);
+        const float beta = __bfloat162float(beta_h);
+        if (threadIdx.x == 0 && rank == 0) beta_out[m] = beta_h;
+        // A3: x_hat = E4M3_RN_satfinite(x' / beta)
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const int64_t k = k0 + ((int64_t)j * nt + threadIdx.x) * 8;
+            if (k < k1) {
+                const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&xv[j]);
+                float v[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] = __bfloat162float(h[i]);
+                uint2 o;
+                o.x = e4m3x2_rn(__fdiv_rn(v[0], beta), __fdiv_rn(v[1], beta)) |
+                      (e4m3x2_rn(__fdiv_rn(v[2], beta), __fdiv_rn(v[3], beta)) << 16);
+                o.y = e4m3x2_rn(__fdiv_rn(v[4], beta), __fdiv_rn(v[5], beta)) |
+                      (e4m3x2_rn(__fdiv_rn(v[6], beta), __fdiv_rn(v[7], beta)) << 16);
+                *reinterpret_cast<uint2*>(xq + m * K + k) = o;
+            }
+        }
+        __syncthreads();                       // red[] reuse by the next row
     }
-    // A2: beta = bf16_RN(amax / 448) (fp32 division then RNE; equals exact RNE for bf16 operands)
-    const __nv_bfloat16 beta_h = amax > 0.0f ? __float2bfloat16_rn(__fdiv_rn(amax, 448.0f))
-                                             : __float2bfloat16_rn(1.0f);
-    const float beta = __bfloat162float(beta_h);
-    if (threadIdx.x == 0 && rank == 0) beta_out[m] = beta_h;
-    // A3: x_hat = E4M3_RN_satfinite(x' / beta)
-    for (int64_t k = k0 + (int64_t)threadIdx.x * 8; k < k1; k += kThreads * 8) {
-        float v[8];
-        load8(s, m, k, v);
-        uint2 o;
-        o.x = e4m3x2_rn(__fdiv_rn(v[0], beta), __fdiv_rn(v[1], beta)) |
-              (e4m3x2_rn(__fdiv_rn(v[2], beta), __fdiv_rn(v[3], beta)) << 16);
-        o.y = e4m3x2_rn(__fdiv_rn(v[4], beta), __fdiv_rn(v[5], beta)) |
-              (e4m3x2_rn(__fdiv_rn(v[6], beta), __fdiv_rn(v[7], beta)) << 16);
-        *reinterpret_cast<uint2*>(xq + m * K + k) = o;
-    }
-    __syncthreads();                       // red[] reuse by the next row
-    }
+}
+
+template <int R>
+cudaError_t launch_act(const Src& s, int64_t M, int64_t K, int cl, int threads, uint8_t* xq, __nv_bfloat16* beta,
+                       cudaStream_t stream) {
+    const unsigned rows = (unsigned)std::min<int64_t>(M, 65535);
+    return launch_ex(k_act_quant<R>, dim3((unsigned)cl, rows), dim3(threads), 0, stream, (unsigned)cl, s, M, K, cl,
+                     xq, beta);
 }
 
 }  // namespace
@@ -134,9 +158,17 @@ fireq_status_t quantize_act_impl(const __nv_bfloat16* X, const __nv_bfloat16* U,
                                  __nv_bfloat16* beta, cudaStream_t stream) {
     Src s{X, U, c, mode, transposed ? 1 : 0, ld};
     const int cl = M <= 64 ? 8 : 1;
-    const unsigned rows = (unsigned)std::min<int64_t>(M, 65535);
-    const cudaError_t e = launch_ex(k_act_quant, dim3((unsigned)cl, rows), dim3(kThreads), 0, stream,
-                                    (unsigned)cl, s, M, K, cl, xq, beta);
+    const int64_t vecs = (K / cl + 7) / 8;
+    // enough threads that each keeps <= 4 vectors (32 values) in registers
+    const int threads = cl > 1 ? 128 : (int)std::min<int64_t>(1024, std::max<int64_t>(128, ((vecs + 3) / 4 + 31) / 32 * 32));
+    const int64_t per = (vecs + threads - 1) / threads;
+    cudaError_t e;
+    if (per <= 1) e = launch_act<1>(s, M, K, cl, threads, xq, beta, stream);
+    else if (per <= 2) e = launch_act<2>(s, M, K, cl, threads, xq, beta, stream);
+    else if (per <= 4) e = launch_act<4>(s, M, K, cl, threads, xq, beta, stream);
+    else if (per <= 8) e = launch_act<8>(s, M, K, cl, threads, xq, beta, stream);
+    else if (per <= 16) e = launch_act<16>(s, M, K, cl, threads, xq, beta, stream);
+    else e = launch_act<32>(s, M, K, cl, threads, xq, beta, stream);
     if (e != cudaSuccess) return fail(FIREQ_ERROR_CUDA, std::string("act quant launch: ") + cudaGetErrorString(e));
     return check_launch(mode == 2 ? "fireq_silu_mul_quantize_act" : "fireq_quantize_act");
 }
