@@ -667,20 +667,26 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                 ptx::named_bar_sync(1, 128);
                 if (misc[1] && C::kFixSlots > 0) {
                     // Stage the contributors' partials (contiguous kPartBytes blocks) into SMEM
-                    // with bulk copies, kFixSlots per round trip, and sum them in CTA order.
+                    // with bulk copies and sum them in CTA order.  After this CTA's last segment
+                    // the weight ring is idle, so it takes all contributors in one round trip.
                     asm volatile("fence.proxy.async.global;" ::: "memory");
+                    SegIter peek = it;
+                    int pt, pg0, pg1;
+                    const bool last_seg = !peek.next(pt, pg0, pg1);
+                    float* fixbuf = last_seg ? reinterpret_cast<float*>(sW) : sFix;
+                    const int slots = last_seg ? (STAGES * C::kWStage) / C::kPartBytes : C::kFixSlots;
                     float accv[C::kFixSlots > 0 ? NTOK : 1];
 #pragma unroll
                     for (int c = 0; c < NTOK; ++c) accv[c] = 0.0f;
-                    for (int cc0 = c_lo; cc0 <= c_hi; cc0 += (C::kFixSlots > 0 ? C::kFixSlots : 1)) {
-                        const int nb = min(C::kFixSlots, c_hi - cc0 + 1);
+                    for (int cc0 = c_lo; cc0 <= c_hi; cc0 += slots) {
+                        const int nb = min(slots, c_hi - cc0 + 1);
                         if (r < 32 && ptx::elect_one()) {
                             ptx::mbar_arrive_expect_tx(fixbar, nb * C::kPartBytes);
                             for (int q = 0; q < nb; ++q) {
                                 const int cc = cc0 + q;
                                 const long long cu0 = (long long)cc * a.U / a.C;
                                 const int sl = 2 * cc + ((cu0 < t0) ? 1 : 0);
-                                ptx::bulk_g2s(sFix + q * (C::kPartBytes / 4), a.partial + (size_t)sl * NTOK * kTileN,
+                                ptx::bulk_g2s(fixbuf + q * (C::kPartBytes / 4), a.partial + (size_t)sl * NTOK * kTileN,
                                               C::kPartBytes, fixbar, 0ull);
                             }
                         }
@@ -689,7 +695,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                         for (int q = 0; q < nb; ++q) {
 #pragma unroll
                             for (int c = 0; c < NTOK; ++c)
-                                accv[c] = __fadd_rn(accv[c], sFix[q * (C::kPartBytes / 4) + c * kTileN + r]);
+                                accv[c] = __fadd_rn(accv[c], fixbuf[q * (C::kPartBytes / 4) + c * kTileN + r]);
                         }
                         ptx::named_bar_sync(1, 128);      // sFix reuse
                     }
