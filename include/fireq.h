@@ -216,6 +216,11 @@ fireq_status_t fireq_debug_lut_table(uint8_t* out, void* stream);
  * start, setup done, first stage landed, MMA issue done, epilogue done, end).
  * Pass NULL to disable.  Not thread-safe; for benchmarks only. */
 fireq_status_t fireq_debug_set_trace(void* buf);
+/* Debug/profiling (profile builds only; no-op otherwise): subsequent launches of the
+ * library record {first CTA start, last CTA end} (%globaltimer ns) into consecutive
+ * slots of the device buffer buf ([cap][2] uint64, caller pre-fills {UINT64_MAX, 0}).
+ * NULL disables.  Not thread-safe; for benchmarks only. */
+fireq_status_t fireq_debug_set_spans(void* buf, int cap);
 /* Number of GEMM kernel launches fireq_w4a8_gemm would enqueue for (M, N, K)
  * and the chosen configuration, for benchmarks: writes {ntok, splits, ctas,
  * sign_split} into cfg_out[4] (host). */

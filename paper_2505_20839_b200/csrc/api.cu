@@ -30,6 +30,13 @@ extern unsigned long long* g_trace;
 
 namespace {
 thread_local std::string g_last_error;
+unsigned long long* g_spans = nullptr;
+int g_span_next = 0, g_span_cap = 0;
+}
+
+unsigned long long* next_span_slot() {
+    if (!g_spans || g_span_next >= g_span_cap) return nullptr;
+    return g_spans + 2 * (g_span_next++);
 }
 
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -207,6 +214,15 @@ fireq_status_t fireq_debug_lut_table(uint8_t* out, void* stream) {
 // ([ctas][8] u64: start, setup done, first stage landed, MMA done, epilogue done, end).
 fireq_status_t fireq_debug_set_trace(void* buf) {
     g_trace = static_cast<unsigned long long*>(buf);
+    return FIREQ_SUCCESS;
+}
+
+// Debug/profiling (profile builds): launches record {start, end} spans into buf
+// ([cap][2] uint64, pre-filled by the caller with {~0, 0}); NULL disables.
+fireq_status_t fireq_debug_set_spans(void* buf, int cap) {
+    g_spans = static_cast<unsigned long long*>(buf);
+    g_span_next = 0;
+    g_span_cap = buf ? cap : 0;
     return FIREQ_SUCCESS;
 }
 

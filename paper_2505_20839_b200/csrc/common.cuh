@@ -45,6 +45,29 @@ cudaError_t launch_ex(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// --------------------------------------------------------------- span tracing
+// Profile builds (FIREQ_PROFILE=1): when enabled with fireq_debug_set_spans, every
+// launch records {min CTA start, max CTA end} (%globaltimer ns) into the next slot.
+unsigned long long* next_span_slot();
+#ifndef FIREQ_PROFILE
+#define FIREQ_PROFILE 0
+#endif
+__device__ __forceinline__ unsigned long long span_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void span_begin(unsigned long long* sp) {
+#if FIREQ_PROFILE
+    if (sp && threadIdx.x == 0) atomicMin(sp, span_now());
+#endif
+}
+__device__ __forceinline__ void span_end(unsigned long long* sp) {
+#if FIREQ_PROFILE
+    if (sp && threadIdx.x == 0) atomicMax(sp + 1, span_now());
+#endif
+}
+
 // --------------------------------------------------------------- device math
 // E4M3 code -> float, from the bit fields (exact).
 __device__ __forceinline__ float e4m3_decode(uint32_t c) {

@@ -65,6 +65,7 @@ struct GemmArgs {
     long long U;           // stream-K units = R * G
     unsigned long long* trace;   // debug timeline [C][8] (%globaltimer ns) or nullptr
     int dbg;                     // experiments only: bit0 skip conversion, bit1 skip MMAs, bit2 skip loads
+    unsigned long long* span;    // profile builds: {start, end} of this launch
 };
 
 // FIREQ_PROFILE=1 builds (scripts/trace_gemm.py) record per-role cycle counters and a
@@ -312,6 +313,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
     constexpr int kWMma = kWEpi + 7;            // MMA issuer
 
     // ------------------------------------------------------------ setup
+    span_begin(a.span);
     if (threadIdx.x == 0) FIREQ_TRACE(0);
     if (warp == kWProdW) ptx::pdl_trigger();   // the next kernel may start its prologue
     if (warp == kWProdW && lane == 0) {
@@ -755,6 +757,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
     ptx::tc_fence_after();
     if (warp == kWAlloc) ptx::tmem_dealloc(tmem, C::kTmemCols);
     if (threadIdx.x == 0) FIREQ_TRACE(5);
+    span_end(a.span);
 }
 
 __global__ void k_lut_table(uint8_t* out) {
@@ -895,6 +898,7 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
     args.C = p.C;
     args.U = p.U;
     args.trace = g_trace;
+    args.span = next_span_slot();
     {
         static const int dbg = getenv("FIREQ_DEBUG_MODE") ? atoi(getenv("FIREQ_DEBUG_MODE")) : 0;
         args.dbg = dbg;

@@ -83,8 +83,10 @@ __device__ __forceinline__ uint4 xprime8(const Src& s, int64_t m, int64_t k) {
 template <int R>
 __global__ void __launch_bounds__(1024) k_act_quant(Src s, int64_t M, int64_t K, int cl,
                                                    uint8_t* __restrict__ xq,
-                                                   __nv_bfloat16* __restrict__ beta_out) {
+                                                   __nv_bfloat16* __restrict__ beta_out,
+                                                   unsigned long long* span) {
     __shared__ float red[32];
+    span_begin(span);
     ptx::pdl_trigger();
     ptx::pdl_wait();                       // X / G / U come from the previous kernel
     const int rank = cl > 1 ? (int)ptx::cluster_ctarank() : 0;
@@ -141,6 +143,7 @@ __global__ void __launch_bounds__(1024) k_act_quant(Src s, int64_t M, int64_t K,
         }
         __syncthreads();                       // red[] reuse by the next row
     }
+    span_end(span);
 }
 
 template <int R>
@@ -148,7 +151,7 @@ cudaError_t launch_act(const Src& s, int64_t M, int64_t K, int cl, int threads, 
                        cudaStream_t stream) {
     const unsigned rows = (unsigned)std::min<int64_t>(M, 65535);
     return launch_ex(k_act_quant<R>, dim3((unsigned)cl, rows), dim3(threads), 0, stream, (unsigned)cl, s, M, K, cl,
-                     xq, beta);
+                     xq, beta, next_span_slot());
 }
 
 }  // namespace
@@ -157,10 +160,13 @@ fireq_status_t quantize_act_impl(const __nv_bfloat16* X, const __nv_bfloat16* U,
                                  int64_t ld, const __nv_bfloat16* c, int mode, bool transposed, uint8_t* xq,
                                  __nv_bfloat16* beta, cudaStream_t stream) {
     Src s{X, U, c, mode, transposed ? 1 : 0, ld};
-    const int cl = M <= 64 ? 8 : 1;
+    // One CTA per token row (a cluster/DSMEM split of the row measured slower at decode:
+    // cluster launch + two cluster barriers cost more latency than they save).
+    const int cl = 1;
     const int64_t vecs = (K / cl + 7) / 8;
-    // enough threads that each keeps <= 4 vectors (32 values) in registers
-    const int threads = cl > 1 ? 128 : (int)std::min<int64_t>(1024, std::max<int64_t>(128, ((vecs + 3) / 4 + 31) / 32 * 32));
+    // decode-sized M: as many threads as vectors (<= 2 per thread); large M: <= 4 per thread
+    const int64_t want = M <= 64 ? (vecs + 1) / 2 : (vecs + 3) / 4;
+    const int threads = (int)std::min<int64_t>(1024, std::max<int64_t>(128, (want + 31) / 32 * 32));
     const int64_t per = (vecs + threads - 1) / threads;
     cudaError_t e;
     if (per <= 1) e = launch_act<1>(s, M, K, cl, threads, xq, beta, stream);

@@ -22,7 +22,7 @@ EXPORTS = [
     "fireq_quantize_weight", "fireq_quantize_act", "fireq_silu_mul_quantize_act",
     "fireq_w4a8_gemm", "fireq_comm_get_unique_id", "fireq_comm_init", "fireq_comm_destroy",
     "fireq_w4a8_gemm_colpar", "fireq_debug_lut_table", "fireq_gemm_plan", "fireq_debug_set_trace",
-    "fireq_quantize_act_t", "fireq_silu_mul_quantize_act_t",
+    "fireq_quantize_act_t", "fireq_silu_mul_quantize_act_t", "fireq_debug_set_spans",
 ]
 
 
@@ -60,6 +60,7 @@ def load(path=LIB_PATH):
         "fireq_debug_lut_table": ([P, P], C),
         "fireq_gemm_plan": ([I64, I64, I64, P], C),
         "fireq_debug_set_trace": ([P], C),
+        "fireq_debug_set_spans": ([P, C], C),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -239,6 +240,12 @@ def w4a8_gemm(xq, beta, packed, scales, N, pts_n, gamma=None, out=None, out_layo
 def debug_set_trace(buf):
     """buf: uint64 CUDA tensor [ctas*8] or None."""
     _check(lib().fireq_debug_set_trace(_ptr(buf) if buf is not None else None), "fireq_debug_set_trace")
+
+
+def debug_set_spans(buf):
+    """buf: int64 CUDA tensor [cap, 2] pre-filled with {-1 (= UINT64_MAX), 0}, or None."""
+    _check(lib().fireq_debug_set_spans(_ptr(buf) if buf is not None else None,
+                                       0 if buf is None else buf.shape[0]), "fireq_debug_set_spans")
 
 
 def debug_lut_table(device="cuda"):
