@@ -159,14 +159,18 @@ class FFN:
         self.ws1 = F.Workspace(F.gemm_workspace_bytes(M, 2 * D_FF, D_MODEL), dev)
         self.ws2 = F.Workspace(F.gemm_workspace_bytes(M, D_MODEL, D_FF), dev)
 
-    def step(self, r, stream=None):
+    def step(self, r, stream=None, prefetch=True):
+        """One FFN: each GEMM also streams the next GEMM's weights into L2 once its own loads
+        are issued (gate_up -> this step's down; down -> the next step's gate_up)."""
         F = self.F
         p_gu, s_gu, p_d, s_d = self.rot[r]
+        nxt = self.rot[(r + 1) % len(self.rot)]
         F.quantize_act(self.x, chan_mul=self.c_gu, out=(self.xq, self.beta), stream=stream)
         F.w4a8_gemm(self.xq, self.beta, p_gu, s_gu, 2 * D_FF, self.n_gu, gamma=self.gamma, out=self.gu,
-                    workspace=self.ws1, stream=stream)
+                    workspace=self.ws1, stream=stream, prefetch=(p_d, s_d) if prefetch else None)
         F.silu_mul_quantize_act(self.gu[:, :D_FF], self.gu[:, D_FF:], out=(self.hq, self.hbeta), stream=stream)
-        F.w4a8_gemm(self.hq, self.hbeta, p_d, s_d, D_MODEL, self.n_d, out=self.y, workspace=self.ws2, stream=stream)
+        F.w4a8_gemm(self.hq, self.hbeta, p_d, s_d, D_MODEL, self.n_d, out=self.y, workspace=self.ws2, stream=stream,
+                    prefetch=(nxt[0], nxt[1]) if prefetch else None)
 
     KERNELS_PER_STEP = 4
 

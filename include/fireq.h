@@ -176,6 +176,23 @@ fireq_status_t fireq_w4a8_gemm(const uint8_t* x_fp8, const void* x_scale, int64_
                                void* Y, int64_t ldy, int out_layout,
                                void* workspace, size_t workspace_bytes, void* stream);
 
+/*
+ * fireq_w4a8_gemm_prefetch -- fireq_w4a8_gemm plus an L2 prefetch hint: once each CTA
+ * has issued its own weight loads it streams its share of [next_packed, +bytes) and
+ * [next_scales, +bytes) (the NEXT layer's packed weights / scales, 16-byte aligned,
+ * either may be NULL) into L2 (cp.async.bulk.prefetch.L2), so that HBM stays busy
+ * through this GEMM's tail and the small kernels that follow and the next GEMM's
+ * weights come from L2.  A performance hint only: results are identical.
+ */
+fireq_status_t fireq_w4a8_gemm_prefetch(const uint8_t* x_fp8, const void* x_scale, int64_t M, int64_t K,
+                                        const uint8_t* w_packed, const uint8_t* w_scales, int64_t N,
+                                        int32_t pts_exponent, const float* out_chan_scale,
+                                        void* Y, int64_t ldy, int out_layout,
+                                        void* workspace, size_t workspace_bytes,
+                                        const void* next_packed, size_t next_packed_bytes,
+                                        const void* next_scales, size_t next_scales_bytes,
+                                        void* stream);
+
 /* --------------------------------------------------------- multi-GPU layer */
 /* Opaque NCCL communicator wrapper (caller-owned, not thread-safe). */
 typedef struct fireq_comm* fireq_comm_t;

@@ -24,7 +24,8 @@ fireq_status_t gemm_plan(int64_t M, int64_t N, int64_t K, int32_t* cfg);
 fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int64_t M, int64_t K,
                          const uint8_t* w_packed, const uint8_t* w_scales, int64_t N, int32_t pts_n,
                          const float* gamma, __nv_bfloat16* Y, int64_t ldy, int out_layout, void* ws,
-                         size_t ws_bytes, cudaStream_t stream);
+                         size_t ws_bytes, cudaStream_t stream, const void* pf0, size_t pf0_bytes,
+                         const void* pf1, size_t pf1_bytes);
 fireq_status_t debug_lut_table(uint8_t* out, cudaStream_t stream);
 extern unsigned long long* g_trace;
 
@@ -185,10 +186,11 @@ fireq_status_t fireq_silu_mul_quantize_act_t(const void* Gt, const void* Ut, int
                              static_cast<cudaStream_t>(stream));
 }
 
-fireq_status_t fireq_w4a8_gemm(const uint8_t* x_fp8, const void* x_scale, int64_t M, int64_t K,
-                               const uint8_t* w_packed, const uint8_t* w_scales, int64_t N, int32_t pts_exponent,
-                               const float* out_chan_scale, void* Y, int64_t ldy, int out_layout, void* workspace,
-                               size_t workspace_bytes, void* stream) {
+static fireq_status_t gemm_checked(const uint8_t* x_fp8, const void* x_scale, int64_t M, int64_t K,
+                                   const uint8_t* w_packed, const uint8_t* w_scales, int64_t N, int32_t pts_exponent,
+                                   const float* out_chan_scale, void* Y, int64_t ldy, int out_layout, void* workspace,
+                                   size_t workspace_bytes, void* stream, const void* pf0, size_t pf0_bytes,
+                                   const void* pf1, size_t pf1_bytes) {
     FIREQ_REQUIRE(x_fp8 && x_scale && w_packed && w_scales && Y && workspace, FIREQ_ERROR_INVALID_VALUE,
                   "fireq_w4a8_gemm: NULL required pointer");
     FIREQ_REQUIRE(M >= 1 && M <= (int64_t(1) << 24), FIREQ_ERROR_INVALID_VALUE, "fireq_w4a8_gemm: M must be in [1, 2^24]");
@@ -200,9 +202,30 @@ fireq_status_t fireq_w4a8_gemm(const uint8_t* x_fp8, const void* x_scale, int64_
     FIREQ_REQUIRE(aligned16(x_fp8) && aligned16(w_packed) && aligned16(w_scales) && aligned16(Y) && ldy % 8 == 0 &&
                       (out_layout == 0 ? ldy >= N : ldy >= M),
                   FIREQ_ERROR_MISALIGNED, "fireq_w4a8_gemm: pointers must be 16-byte aligned, ldy % 8 == 0 and large enough");
+    FIREQ_REQUIRE((!pf0 || aligned16(pf0)) && (!pf1 || aligned16(pf1)), FIREQ_ERROR_MISALIGNED,
+                  "fireq_w4a8_gemm_prefetch: prefetch regions must be 16-byte aligned");
     return gemm_impl(x_fp8, static_cast<const __nv_bfloat16*>(x_scale), M, K, w_packed, w_scales, N, pts_exponent,
                      out_chan_scale, static_cast<__nv_bfloat16*>(Y), ldy, out_layout, workspace, workspace_bytes,
-                     static_cast<cudaStream_t>(stream));
+                     static_cast<cudaStream_t>(stream), pf0, pf0_bytes, pf1, pf1_bytes);
+}
+
+fireq_status_t fireq_w4a8_gemm(const uint8_t* x_fp8, const void* x_scale, int64_t M, int64_t K,
+                               const uint8_t* w_packed, const uint8_t* w_scales, int64_t N, int32_t pts_exponent,
+                               const float* out_chan_scale, void* Y, int64_t ldy, int out_layout, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+    return gemm_checked(x_fp8, x_scale, M, K, w_packed, w_scales, N, pts_exponent, out_chan_scale, Y, ldy, out_layout,
+                        workspace, workspace_bytes, stream, nullptr, 0, nullptr, 0);
+}
+
+fireq_status_t fireq_w4a8_gemm_prefetch(const uint8_t* x_fp8, const void* x_scale, int64_t M, int64_t K,
+                                        const uint8_t* w_packed, const uint8_t* w_scales, int64_t N,
+                                        int32_t pts_exponent, const float* out_chan_scale, void* Y, int64_t ldy,
+                                        int out_layout, void* workspace, size_t workspace_bytes,
+                                        const void* next_packed, size_t next_packed_bytes, const void* next_scales,
+                                        size_t next_scales_bytes, void* stream) {
+    return gemm_checked(x_fp8, x_scale, M, K, w_packed, w_scales, N, pts_exponent, out_chan_scale, Y, ldy, out_layout,
+                        workspace, workspace_bytes, stream, next_packed, next_packed_bytes, next_scales,
+                        next_scales_bytes);
 }
 
 fireq_status_t fireq_debug_lut_table(uint8_t* out, void* stream) {

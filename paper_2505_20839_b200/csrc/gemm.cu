@@ -66,6 +66,8 @@ struct GemmArgs {
     unsigned long long* trace;   // debug timeline [C][8] (%globaltimer ns) or nullptr
     int dbg;                     // experiments only: bit0 skip conversion, bit1 skip MMAs, bit2 skip loads
     unsigned long long* span;    // profile builds: {start, end} of this launch
+    const uint8_t* pf_ptr[2];    // L2 prefetch of the next layer's weights (may be null)
+    size_t pf_bytes[2];
 };
 
 // FIREQ_PROFILE=1 builds (scripts/trace_gemm.py) record per-role cycle counters and a
@@ -381,6 +383,20 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
             }
             __syncwarp();
             ++i;
+        }
+        // Once this CTA's own weight loads are issued, stream its share of the NEXT layer's
+        // weights into L2 (caller hint): HBM stays busy through this kernel's tail and the
+        // small kernels that follow, and the next GEMM starts from L2-resident weights.
+        for (int q = 0; q < 2; ++q) {
+            if (!a.pf_ptr[q] || a.pf_bytes[q] == 0) continue;
+            const size_t per = (a.pf_bytes[q] / a.C + 15) & ~size_t(15);
+            const size_t b0 = per * blockIdx.x;
+            const size_t b1 = min(a.pf_bytes[q], b0 + per);
+            if (ptx::elect_one()) {
+                for (size_t off = b0; off < b1; off += 32768)
+                    ptx::bulk_prefetch_l2(a.pf_ptr[q] + off, (uint32_t)min((size_t)32768, b1 - off));
+            }
+            __syncwarp();
         }
     } else if (warp == kWProdX) {
         // ------------------------------------------------------- activation producer
@@ -875,7 +891,8 @@ fireq_status_t gemm_plan(int64_t M, int64_t N, int64_t K, int32_t* cfg) {
 fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int64_t M, int64_t K,
                          const uint8_t* w_packed, const uint8_t* w_scales, int64_t N, int32_t pts_n,
                          const float* gamma, __nv_bfloat16* Y, int64_t ldy, int out_layout, void* ws,
-                         size_t ws_bytes, cudaStream_t stream) {
+                         size_t ws_bytes, cudaStream_t stream, const void* pf0, size_t pf0_bytes,
+                         const void* pf1, size_t pf1_bytes) {
     const Plan p = make_plan(M, N, K);
     if (ws_bytes < gemm_workspace_bytes(M, N, K)) return fail(FIREQ_ERROR_WORKSPACE, "GEMM workspace too small");
     CUtensorMap map;
@@ -898,6 +915,10 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
     args.C = p.C;
     args.U = p.U;
     args.trace = g_trace;
+    args.pf_ptr[0] = static_cast<const uint8_t*>(pf0);
+    args.pf_bytes[0] = pf0 ? (pf0_bytes & ~size_t(15)) : 0;
+    args.pf_ptr[1] = static_cast<const uint8_t*>(pf1);
+    args.pf_bytes[1] = pf1 ? (pf1_bytes & ~size_t(15)) : 0;
     args.span = next_span_slot();
     {
         static const int dbg = getenv("FIREQ_DEBUG_MODE") ? atoi(getenv("FIREQ_DEBUG_MODE")) : 0;

@@ -60,6 +60,10 @@ __device__ __forceinline__ void tma_2d_g2s(void* dst_smem, const CUtensorMap* ma
           "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
+// Prefetch [src, src + bytes) into L2 (no SMEM destination); bytes % 16 == 0.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }

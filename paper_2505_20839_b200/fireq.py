@@ -23,6 +23,7 @@ EXPORTS = [
     "fireq_w4a8_gemm", "fireq_comm_get_unique_id", "fireq_comm_init", "fireq_comm_destroy",
     "fireq_w4a8_gemm_colpar", "fireq_debug_lut_table", "fireq_gemm_plan", "fireq_debug_set_trace",
     "fireq_quantize_act_t", "fireq_silu_mul_quantize_act_t", "fireq_debug_set_spans",
+    "fireq_w4a8_gemm_prefetch",
 ]
 
 
@@ -51,6 +52,7 @@ def load(path=LIB_PATH):
         "fireq_quantize_act": ([P, I64, I64, I64, P, P, P, P], C),
         "fireq_silu_mul_quantize_act": ([P, P, I64, I64, I64, P, P, P], C),
         "fireq_w4a8_gemm": ([P, P, I64, I64, P, P, I64, I32, P, P, I64, C, P, SZ, P], C),
+        "fireq_w4a8_gemm_prefetch": ([P, P, I64, I64, P, P, I64, I32, P, P, I64, C, P, SZ, P, SZ, P, SZ, P], C),
         "fireq_comm_get_unique_id": ([P], C),
         "fireq_comm_init": ([P, C, C, P], C),
         "fireq_comm_destroy": ([P], C),
@@ -223,8 +225,12 @@ class Workspace:
 
 
 def w4a8_gemm(xq, beta, packed, scales, N, pts_n, gamma=None, out=None, out_layout=0, workspace=None,
-              stream=None):
-    """Y = fireq_w4a8_gemm(...): bf16 [M][N] (out_layout 0) or [N][M] (out_layout 1)."""
+              stream=None, prefetch=None):
+    """Y = fireq_w4a8_gemm(...): bf16 [M][N] (out_layout 0) or [N][M] (out_layout 1).
+
+    prefetch: optional (next_packed, next_scales) uint8 tensors of the next layer, streamed
+    into L2 once this GEMM's own weight loads are issued (fireq_w4a8_gemm_prefetch).
+    """
     M, K = xq.shape
     L = lib()
     need = L.fireq_w4a8_gemm_workspace_bytes(M, N, K)
@@ -232,8 +238,16 @@ def w4a8_gemm(xq, beta, packed, scales, N, pts_n, gamma=None, out=None, out_layo
     if out is None:
         out = torch.empty((M, N) if out_layout == 0 else (N, M), dtype=torch.bfloat16, device=xq.device)
     ldy = out.stride(0)
-    _check(L.fireq_w4a8_gemm(_ptr(xq), _ptr(beta), M, K, _ptr(packed), _ptr(scales), N, pts_n, _ptr(gamma),
-                             _ptr(out), ldy, out_layout, _ptr(ws), ws.numel(), _stream(stream)), "fireq_w4a8_gemm")
+    if prefetch is None:
+        _check(L.fireq_w4a8_gemm(_ptr(xq), _ptr(beta), M, K, _ptr(packed), _ptr(scales), N, pts_n, _ptr(gamma),
+                                 _ptr(out), ldy, out_layout, _ptr(ws), ws.numel(), _stream(stream)), "fireq_w4a8_gemm")
+    else:
+        pp, ps = prefetch
+        _check(L.fireq_w4a8_gemm_prefetch(_ptr(xq), _ptr(beta), M, K, _ptr(packed), _ptr(scales), N, pts_n,
+                                          _ptr(gamma), _ptr(out), ldy, out_layout, _ptr(ws), ws.numel(),
+                                          _ptr(pp), pp.numel() if pp is not None else 0,
+                                          _ptr(ps), ps.numel() if ps is not None else 0, _stream(stream)),
+               "fireq_w4a8_gemm_prefetch")
     return out
 
 
