@@ -238,9 +238,10 @@ fireq_status_t fireq_debug_set_trace(void* buf);
  * slots of the device buffer buf ([cap][2] uint64, caller pre-fills {UINT64_MAX, 0}).
  * NULL disables.  Not thread-safe; for benchmarks only. */
 fireq_status_t fireq_debug_set_spans(void* buf, int cap);
-/* Number of GEMM kernel launches fireq_w4a8_gemm would enqueue for (M, N, K)
- * and the chosen configuration, for benchmarks: writes {ntok, splits, ctas,
- * sign_split} into cfg_out[4] (host). */
+/* The schedule fireq_w4a8_gemm chooses for (M, N, K), for benchmarks and tests:
+ * writes {ntok, mode, ctas, sign_split} into cfg_out[4] (host).  mode 0 = whole
+ * tiles, 1 = whole tiles + stream-K remainder (global-memory fixup), 2 = cluster
+ * split-K (ctas / tiles CTAs per tile, DSMEM reduction). */
 fireq_status_t fireq_gemm_plan(int64_t M, int64_t N, int64_t K, int32_t cfg_out[4]);
 
 #ifdef __cplusplus

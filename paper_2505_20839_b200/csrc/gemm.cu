@@ -63,6 +63,7 @@ struct GemmArgs {
     int R;                 // tiles [0, R) are split contiguously over CTAs ("stream-K")
     int C;                 // CTAs in the grid
     long long U;           // stream-K units = R * G
+    int S;                 // > 1: cluster split-K, one tile per cluster of S CTAs (K split S ways)
     unsigned long long* trace;   // debug timeline [C][8] (%globaltimer ns) or nullptr
     int dbg;                     // experiments only: bit0 skip conversion, bit1 skip MMAs, bit2 skip loads
     unsigned long long* span;    // profile builds: {start, end} of this launch
@@ -104,14 +105,23 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // [0, R) (so that split tiles are reduced early, overlapped with later work), then the
 // whole tiles R + c, R + c + C, ...
 struct SegIter {
-    int G, tiles, C, c, R, k;
+    int G, tiles, C, c, R, k, S;
     long long u, u_end;
     __device__ __forceinline__ void init(const GemmArgs& a, int cta) {
-        G = a.G; tiles = a.tiles; C = a.C; c = cta; R = a.R; k = 0;
+        G = a.G; tiles = a.tiles; C = a.C; c = cta; R = a.R; k = 0; S = a.S;
         u = a.U ? (long long)cta * a.U / a.C : 0;
         u_end = a.U ? (long long)(cta + 1) * a.U / a.C : 0;
     }
     __device__ __forceinline__ bool next(int& tile, int& g0, int& g1) {
+        if (S > 1) {
+            // cluster split-K: CTA rank q of cluster t takes groups [q G / S, (q + 1) G / S) of tile t
+            if (k++) return false;
+            const int q = c % S;
+            tile = c / S;
+            g0 = q * G / S;
+            g1 = (q + 1) * G / S;
+            return true;
+        }
         if (u < u_end) {
             tile = (int)(u / G);
             g0 = (int)(u % G);
@@ -348,6 +358,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
+    if (a.S > 1) ptx::cluster_sync();       // peers' mbarrier inits visible before any st.async
     const uint32_t tmem = misc[0];
     if (threadIdx.x == 0) FIREQ_TRACE(1);
 
@@ -634,12 +645,27 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
             gam = a.gamma ? a.gamma[n] : 1.0f;
             for (int t = r; t < NTOK; t += 128)
                 sScale[t] = (m0 + t < a.M) ? __fmul_rn(__bfloat162float(a.x_scale[m0 + t]), p2) : 0.0f;
-            const bool whole = (g0 == 0 && g1 == a.G);
+            const bool csplit = a.S > 1;
+            const bool whole = (g0 == 0 && g1 == a.G) || csplit;
+            // cluster split-K: rank 0 sums the ranks' partials in rank order; the other ranks
+            // push theirs into rank 0's sFix slot q - 1 ([r][NTOK] fp32, 16-B units XOR-swizzled)
+            const int cq = csplit ? (int)(blockIdx.x % a.S) : 0;
+            const int swz = NTOK == 16 ? ((r >> 1) & 3) : (r & 7);
             int slot = 0;
             if (!whole) slot = 2 * blockIdx.x + ((u_first < (long long)tile * a.G) ? 1 : 0);   // first/last segment
             float* part = a.partial + (size_t)slot * NTOK * kTileN;
+            uint32_t peer_dst = 0, peer_bar = 0;
+            if (C::kFixSlots > 0 && csplit) {
+                if (cq == 0) {
+                    if (r == 0) ptx::mbar_arrive_expect_tx(fixbar, (a.S - 1) * C::kPartBytes);
+                } else {
+                    peer_dst = ptx::mapa_shared(ptx::smem_u32(sFix) + (cq - 1) * C::kPartBytes + r * NTOK * 4, 0);
+                    peer_bar = ptx::mapa_shared(ptx::smem_u32(fixbar), 0);
+                }
+            }
             ptx::mbar_wait(&accfull[b], (sg / ACCBUF) & 1);
             ptx::tc_fence_after();
+            if (C::kFixSlots > 0 && csplit && cq == 0) ptx::mbar_wait(fixbar, 0);
             ptx::named_bar_sync(1, 128);            // sScale visible
 #pragma unroll 1
             for (int ch = 0; ch < NTOK / 16; ++ch) {
@@ -656,10 +682,28 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                 } else {
                     ptx::tmem_wait_ld();
                 }
-                if (whole) {
+                if (C::kFixSlots > 0 && csplit && cq != 0) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        ptx::st_async_v4(peer_dst + (((ch * 4 + j) ^ swz) * 16), v[4 * j], v[4 * j + 1], v[4 * j + 2],
+                                         v[4 * j + 3], peer_bar);
+                } else if (whole) {
                     float accv[16];
 #pragma unroll
                     for (int c = 0; c < 16; ++c) accv[c] = __uint_as_float(v[c]);
+                    if (C::kFixSlots > 0 && csplit) {
+                        for (int q = 1; q < a.S; ++q) {
+                            const float* src = sFix + (q - 1) * (C::kPartBytes / 4) + r * NTOK;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const float4 f = *reinterpret_cast<const float4*>(src + ((ch * 4 + j) ^ swz) * 4);
+                                accv[4 * j] = __fadd_rn(accv[4 * j], f.x);
+                                accv[4 * j + 1] = __fadd_rn(accv[4 * j + 1], f.y);
+                                accv[4 * j + 2] = __fadd_rn(accv[4 * j + 2], f.z);
+                                accv[4 * j + 3] = __fadd_rn(accv[4 * j + 3], f.w);
+                            }
+                        }
+                    }
                     emit(accv, ch);
                 } else {
 #pragma unroll
@@ -826,7 +870,7 @@ bool make_x_map(CUtensorMap* out, const uint8_t* x, int64_t M, int64_t K, int nt
 }
 
 struct Plan {
-    int ntok, m_tiles, n_tiles, tiles, G, mode, C, R;
+    int ntok, m_tiles, n_tiles, tiles, G, mode, C, R, S;
     long long U;
     bool sign_split;
 };
@@ -852,6 +896,22 @@ Plan make_plan(int64_t M, int64_t N, int64_t K) {
     }
     p.U = (long long)p.R * p.G;
     p.mode = p.R > 0 ? 1 : 0;
+    p.S = 1;
+    // Few tiles (decode-sized N): split K over a cluster of S CTAs per tile and reduce the
+    // partials through DSMEM instead of stream-K's global-memory fixup (no second round trip
+    // through L2 on the critical path).  S - 1 partials must fit the receiver's fixup buffer.
+    static const bool no_csplit = getenv("FIREQ_NO_CSPLIT") != nullptr;
+    const int slots = p.ntok <= 32 ? 32768 / (p.ntok * kTileN * 4) : 0;
+    if (!no_csplit && slots > 0 && 2 * p.tiles <= sms) {
+        const int S = std::min(std::min(sms / p.tiles, 8), std::min(slots + 1, p.G));
+        if (S > 1) {
+            p.S = S;
+            p.mode = 2;
+            p.R = 0;
+            p.U = 0;
+            p.C = p.tiles * S;
+        }
+    }
     return p;
 }
 
@@ -865,7 +925,8 @@ fireq_status_t launch_cfg(const CUtensorMap& map, const GemmArgs& args, cudaStre
             return fail(FIREQ_ERROR_CUDA, "cudaFuncSetAttribute(smem) failed");
         attr_done = true;
     }
-    const cudaError_t e = launch_ex(kern, dim3(args.C), dim3(C::kThreads), C::kSmemBytes, stream, 1u, map, args);
+    const cudaError_t e = launch_ex(kern, dim3(args.C), dim3(C::kThreads), C::kSmemBytes, stream,
+                                    (unsigned)(args.S > 1 ? args.S : 1), map, args);
     if (e != cudaSuccess) return fail(FIREQ_ERROR_CUDA, std::string("fireq_w4a8_gemm launch: ") + cudaGetErrorString(e));
     return check_launch("fireq_w4a8_gemm");
 }
@@ -914,6 +975,7 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
     args.R = p.R;
     args.C = p.C;
     args.U = p.U;
+    args.S = p.S;
     args.trace = g_trace;
     args.pf_ptr[0] = static_cast<const uint8_t*>(pf0);
     args.pf_bytes[0] = pf0 ? (pf0_bytes & ~size_t(15)) : 0;

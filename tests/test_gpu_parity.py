@@ -171,6 +171,21 @@ def test_gemm_g4(fireq, M, N, K):
     assert og.rel_frobenius(y, r) < 5e-3
 
 
+@pytest.mark.parametrize("M,N,K,mode", [
+    (16, 10240, 256, "stream-k"),            # 80 tiles: stream-K remainder over all CTAs
+    (16, 4096, 1280, "cluster-split-k"),     # 32 tiles x 4-CTA clusters, ragged K split (10 / 4)
+    (32, 256, 2048, "cluster-split-k"),      # NTOK 32: 3-CTA clusters, 16 groups / 3
+    (5, 128, 640, "cluster-split-k"),        # one tile, 5 groups over 5 CTAs
+])
+def test_gemm_schedules(fireq, M, N, K, mode):
+    """Each schedule of make_plan against the oracle, all output elements."""
+    plan = fireq.gemm_plan(M, N, K)
+    assert plan["mode"] == mode, plan          # schedules as chosen on a 148-SM B200
+    y, r, *_ = run_case(fireq, M, N, K, seed=N + K)
+    assert og.g4_error(y, r) <= G4_TOL
+    assert og.rel_frobenius(y, r) < 5e-3
+
+
 @pytest.mark.parametrize("M", [16, 200])
 def test_gemm_transposed_output_and_gamma(fireq, M):
     y, r, *_ = run_case(fireq, M, 256, 512, gamma=True, out_layout=1, seed=M)
