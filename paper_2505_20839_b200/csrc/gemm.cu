@@ -64,8 +64,9 @@ struct GemmArgs {
     int C;                 // CTAs in the grid
     long long U;           // stream-K units = R * G
     int S;                 // > 1: cluster split-K, one tile per cluster of S CTAs (K split S ways)
+    int depth;             // weight stages in flight (<= STAGES): bounds the loaded HBM latency
     unsigned long long* trace;   // debug timeline [C][8] (%globaltimer ns) or nullptr
-    int dbg;                     // experiments only: bit0 skip conversion, bit1 skip MMAs, bit2 skip loads
+    int dbg;                     // experiments only: bit0 skip conversion, bit1 skip MMAs, bit2 skip weight loads
     unsigned long long* span;    // profile builds: {start, end} of this launch
     const uint8_t* pf_ptr[2];    // L2 prefetch of the next layer's weights (may be null)
     size_t pf_bytes[2];
@@ -94,10 +95,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // per-stage event log of CTA 0: trace[C*16 + stage*8 + ev] (first 64 stages)
 #define FIREQ_EVT(stage, ev) do { if (a.trace && blockIdx.x == 0 && (stage) < 64) \
     a.trace[a.C * 16 + (stage) * 8 + (ev)] = clock64(); } while (0)
+// second per-CTA timeline (epilogue): trace[C*16 + 512 + cta*16 + slot]
+#define FIREQ_TRACE2(slot) do { if (a.trace && (slot) < 16) \
+    a.trace[a.C * 16 + 512 + blockIdx.x * 16 + (slot)] = gtimer(); } while (0)
 #else
 #define FIREQ_TRACE(slot) do { } while (0)
 #define FIREQ_TRACE_VAL(slot, v) do { } while (0)
 #define FIREQ_EVT(stage, ev) do { } while (0)
+#define FIREQ_TRACE2(slot) do { } while (0)
 #endif
 
 // Segment = contiguous run of groups [g0, g1) of one tile processed by one CTA.
@@ -290,7 +295,7 @@ __device__ __forceinline__ void conv_mask_select(uint32_t w, uint32_t L0, uint32
 // allocator, activation TMA producer (the only role that waits on the previous kernel,
 // PDL), weight TMA producer, MMA issuer.
 template <int NTOK, bool SIGN_SPLIT, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS, int NMMA>
-__global__ void __maxnreg__((NTOK <= 32 ? 88 : NTOK <= 64 ? 96 : 128))
+__global__ void __maxnreg__((NCONV >= 4 ? 80 : NTOK <= 32 ? 88 : NTOK <= 64 ? 96 : 128))
 k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
     using C = Cfg<NTOK, SIGN_SPLIT, NCONV, STAGES, ASTAGES, ACCBUF, GPS, NMMA>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -330,7 +335,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
     if (warp == kWProdW) ptx::pdl_trigger();   // the next kernel may start its prologue
     if (warp == kWProdW && lane == 0) {
         for (int i = 0; i < STAGES; ++i) {
-            ptx::mbar_init(&fullW[i], 2);       // weight producer + activation producer
+            ptx::mbar_init(&fullW[i], 1);
             ptx::mbar_init(&fullX[i], 1);
             ptx::mbar_init(&empty[i], 1);
         }
@@ -381,6 +386,15 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
         while (st.next(nt, mt, g, ng, sfirst, slast)) {
             const int s = i % STAGES;
             ptx::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+            // Keep at most `depth` stages in flight: past the point where HBM is saturated,
+            // more outstanding bytes only lengthen the queue every other global access of
+            // this kernel (epilogue stores, fixup loads) waits in.  Completion of stage j
+            // implies completion of every stage <= j - 2 (per-issuer order + the converters'
+            // A-ring wait), so depth <= STAGES - 2 also frees slot s.
+            if (a.depth < STAGES && i >= a.depth) {
+                const int j = i - a.depth;
+                ptx::mbar_wait(&empty[j % STAGES], (j / STAGES) & 1);
+            }
             if (lane == 0) FIREQ_EVT(i, 0);
             if (ptx::elect_one()) {
                 if (a.dbg & 4) {
@@ -421,16 +435,12 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
             const int s = i % STAGES;
             ptx::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
             if (ptx::elect_one()) {
-                if (a.dbg & 4) {
-                    ptx::mbar_arrive(&fullW[s]);
-                } else {
-                    // same barrier as the weights (arrival count 2): the converters wait on it,
-                    // and the MMA issuer, which waits on the converters, needs no extra wait.
-                    ptx::mbar_arrive_expect_tx(&fullW[s], ng * C::kXBytes);
-                    for (int q = 0; q < ng; ++q)
-                        ptx::tma_2d_g2s(sX + s * C::kXStage + q * C::kXBytes, &tmap_x, (g + q) * kGroup, mt * NTOK,
-                                        &fullW[s], pol_x);
-                }
+                // own barrier: the converters need only the weights, so they run ahead of the
+                // previous kernel (PDL) and fill the TMEM A ring before the activations land
+                ptx::mbar_arrive_expect_tx(&fullX[s], ng * C::kXBytes);
+                for (int q = 0; q < ng; ++q)
+                    ptx::tma_2d_g2s(sX + s * C::kXStage + q * C::kXBytes, &tmap_x, (g + q) * kGroup, mt * NTOK,
+                                    &fullX[s], pol_x);
             }
             __syncwarp();
             ++i;
@@ -464,6 +474,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                 ptx::mbar_wait(&afull[as], (i / ASTAGES) & 1);
                 if (lane == 0) FIREQ_EVT(i, 4);
                 const long long c1 = prof_clock();
+                ptx::mbar_wait(&fullX[s], (i / STAGES) & 1);
                 if (lane == 0) FIREQ_EVT(i, 5);
                 w_afull += c1 - c0;
                 w_full += prof_clock() - c1;
@@ -514,11 +525,15 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
         const int wg = warp >> 2;                 // converter warpgroup
         const int r = threadIdx.x & 127;          // weight row == TMEM lane
         const uint32_t lane_base = (uint32_t)(r & ~31) << 16;
-        st.init(a, blockIdx.x);
-        int i = 0;
+        // The converters only need the number of stages: a stage's weights sit in SMEM slot
+        // i % STAGES whatever its tile, and a short last stage of a segment (ng < GPS) is
+        // converted in full (the stale SMEM group lands in TMEM columns no MMA reads), so the
+        // group loop is fully unrolled and warpgroup wg walks only its own stages.
+        int n_stages = 0;
+        it.init(a, blockIdx.x);
+        while (it.next(tile, g0, g1)) n_stages += (g1 - g0 + GPS - 1) / GPS;
         long long cw_full = 0, cw_aempty = 0, ct0 = prof_clock();
-        while (st.next(nt, mt, g, ng, sfirst, slast)) {
-            if ((i % NCONV) != wg) { ++i; continue; }
+        for (int i = wg; i < n_stages; i += NCONV) {
             const int s = i % STAGES, as = i % ASTAGES;
             const long long c0 = prof_clock();
             ptx::mbar_wait(&fullW[s], (i / STAGES) & 1);
@@ -539,8 +554,9 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
             ptx::tc_fence_after();
             if (!(a.dbg & 1)) {
                 const uint32_t ta = tmem + lane_base + C::kACol0 + as * C::kASz;
-                for (int q = 0; q < ng; ++q) {
-                    const uint4 L = sLut[sS[s * C::kSStage + q * kTileN + r]];
+#pragma unroll
+                for (int q = 0; q < GPS; ++q) {
+                    const uint4 L = sLut[sS[s * C::kSStage + q * kTileN + r] & 0x7F];
                     const uint8_t* wrow = sW + s * C::kWStage + q * kWBytes + r * 16;
                     if (SIGN_SPLIT) {
                         const uint32_t N0 = L.z & 0x7F7F7F7Fu, N1 = L.w & 0x7F7F7F7Fu;
@@ -574,7 +590,6 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&afull[as]);
             if (r == 0) FIREQ_EVT(i, 3);
-            ++i;
         }
         if (threadIdx.x == 0) {
             FIREQ_TRACE_VAL(12, cw_full);
@@ -665,7 +680,11 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
             }
             ptx::mbar_wait(&accfull[b], (sg / ACCBUF) & 1);
             ptx::tc_fence_after();
-            if (C::kFixSlots > 0 && csplit && cq == 0) ptx::mbar_wait(fixbar, 0);
+            if (r == 0 && sg < 4) FIREQ_TRACE2(3 * sg);
+            if (C::kFixSlots > 0 && csplit && cq == 0) {
+                ptx::mbar_wait(fixbar, 0);
+                if (r == 0) FIREQ_TRACE2(12);
+            }
             ptx::named_bar_sync(1, 128);            // sScale visible
 #pragma unroll 1
             for (int ch = 0; ch < NTOK / 16; ++ch) {
@@ -720,11 +739,13 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                 const long long t0 = (long long)tile * a.G, t1 = t0 + a.G - 1;
                 const int c_lo = owner_of(t0, a.U, a.C), c_hi = owner_of(t1, a.U, a.C);
                 if (r == 0) {
+                    if (sg == 0) FIREQ_TRACE2(10);
                     // gpu-scope acq_rel: publishes this CTA's partials (bar.sync cumulativity)
                     // and, for the last arriver, acquires everyone else's.
                     unsigned prev;
                     asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&a.counters[tile]) : "memory");
                     misc[1] = (prev == (unsigned)(c_hi - c_lo)) ? 1u : 0u;
+                    if (sg < 4) FIREQ_TRACE2(3 * sg + 1);
                 }
                 ptx::named_bar_sync(1, 128);
                 if (misc[1] && C::kFixSlots > 0) {
@@ -806,6 +827,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                 }
                 ptx::named_bar_sync(1, 128);
             }
+            if (r == 0 && sg < 4) FIREQ_TRACE2(3 * sg + 2);
             ++sg;
         }
     }
@@ -925,8 +947,10 @@ fireq_status_t launch_cfg(const CUtensorMap& map, const GemmArgs& args, cudaStre
             return fail(FIREQ_ERROR_CUDA, "cudaFuncSetAttribute(smem) failed");
         attr_done = true;
     }
-    const cudaError_t e = launch_ex(kern, dim3(args.C), dim3(C::kThreads), C::kSmemBytes, stream,
-                                    (unsigned)(args.S > 1 ? args.S : 1), map, args);
+    GemmArgs la = args;
+    if (la.depth > STAGES - 2 || la.depth < 1) la.depth = STAGES;
+    const cudaError_t e = launch_ex(kern, dim3(la.C), dim3(C::kThreads), C::kSmemBytes, stream,
+                                    (unsigned)(la.S > 1 ? la.S : 1), map, la);
     if (e != cudaSuccess) return fail(FIREQ_ERROR_CUDA, std::string("fireq_w4a8_gemm launch: ") + cudaGetErrorString(e));
     return check_launch("fireq_w4a8_gemm");
 }
@@ -976,6 +1000,10 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
     args.C = p.C;
     args.U = p.U;
     args.S = p.S;
+    {
+        static const int depth = getenv("FIREQ_DEPTH") ? atoi(getenv("FIREQ_DEPTH")) : 1000;   // experiments
+        args.depth = depth;
+    }
     args.trace = g_trace;
     args.pf_ptr[0] = static_cast<const uint8_t*>(pf0);
     args.pf_bytes[0] = pf0 ? (pf0_bytes & ~size_t(15)) : 0;
@@ -992,7 +1020,16 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
         // decode configs: >= 128 KB of weights in flight per SM (hides the loaded DRAM
         // latency), 2 groups per stage (halves the per-stage synchronisation cost), and
         // <= 96 registers per thread so a CTA of the next small kernel of a PDL chain fits.
-        case 16:  return launch_cfg<16, true, 3, 8, 3, 2, 2, 2>(map, args, stream);
+        case 16: {
+            static const int v = getenv("FIREQ_CFG16") ? atoi(getenv("FIREQ_CFG16")) : 0;   // experiments
+            switch (v) {
+                case 1: return launch_cfg<16, true, 3, 16, 7, 2, 1, 2>(map, args, stream);
+                case 2: return launch_cfg<16, true, 4, 16, 7, 2, 1, 2>(map, args, stream);
+                case 3: return launch_cfg<16, false, 3, 8, 7, 2, 2, 2>(map, args, stream);
+                case 4: return launch_cfg<16, false, 4, 8, 7, 2, 2, 2>(map, args, stream);
+                default: return launch_cfg<16, true, 3, 8, 3, 2, 2, 2>(map, args, stream);
+            }
+        }
         case 32:  return launch_cfg<32, true, 3, 7, 3, 2, 2, 1>(map, args, stream);
         case 64:  return launch_cfg<64, true, 2, 5, 2, 2, 2, 1>(map, args, stream);
         case 128: return launch_cfg<128, true, 2, 7, 4, 2, 1, 1>(map, args, stream);

@@ -17,7 +17,7 @@ for (M, N, K) in [(16, 22016, 4096), (16, 4096, 11008), (16, 4096, 4096), (16384
     n = qw.n
     plan = F.gemm_plan(M, N, K)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-    tr = torch.zeros(plan["ctas"] * 16 + 512, dtype=torch.int64, device="cuda")
+    tr = torch.zeros(plan["ctas"] * 32 + 512, dtype=torch.int64, device="cuda")
     for it in range(3):
         flush.fill_(it)
         F.debug_set_trace(tr if it == 2 else None)
@@ -44,3 +44,13 @@ for (M, N, K) in [(16, 22016, 4096), (16, 4096, 11008), (16, 4096, 4096), (16384
         print(f"   cyc {nm:18s} med={np.median(cyc[:, j]):9.0f}")
     del W, X, qw, flush
     torch.cuda.empty_cache()
+    if os.environ.get("TRACE_SLOW"):
+        order = np.argsort(-np.nan_to_num(rel[:, 5]))
+        print("   slowest CTAs: cta " + " ".join(f"{n:>10s}" for n in names))
+        for c in order[:12]:
+            print(f"   {c:4d} " + " ".join(f"{v:10.2f}" for v in rel[c]))
+        t2 = tr.cpu().numpy()[plan["ctas"] * 16 + 512:].reshape(-1, 16).astype(np.int64)
+        rel2 = np.where(t2 > 0, (t2 - t0) / 1000.0, np.nan)
+        print("   epilogue per segment: accfull seen / arrived (stream-K) / segment done")
+        for c in order[:12]:
+            print(f"   {c:4d} " + " ".join(f"{v:7.2f}" for v in rel2[c, :12]))
