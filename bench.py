@@ -183,6 +183,45 @@ class FFN:
         return 2 * self.M * (2 * D_FF * D_MODEL + D_MODEL * D_FF)
 
 
+class FusedFFN:
+    """The same FFN through fireq_ffn_w4a8_decode: 3 kernels per step (quantize_act(x);
+    gate_up with the SwiGLU epilogue and h's quantization in its tail; down).  W_gu in
+    the interleaved row order."""
+
+    KERNELS_PER_STEP = 3
+
+    def __init__(self, F, M, rotations, dev):
+        from types import SimpleNamespace as NS
+        self.F, self.M, self.dev = F, M, dev
+        Wg = synth.bits_to_torch(synth.weights(D_FF, D_MODEL, synth.layer_seed(1, 0))).to(dev)
+        Wu = synth.bits_to_torch(synth.weights(D_FF, D_MODEL, synth.layer_seed(1, 1))).to(dev)
+        W_d = synth.bits_to_torch(synth.weights(D_MODEL, D_FF, synth.layer_seed(1, 2))).to(dev)
+        W_il = F.interleave_gate_up(Wg, Wu)
+        q_gu = F.quantize_weight(W_il, cas_mode=1)
+        q_d = F.quantize_weight(W_d, cas_mode=1)
+        del Wg, Wu, W_d, W_il
+        self.rot = []
+        for _ in range(rotations):
+            self.rot.append((NS(packed=q_gu.packed.clone(), scales=q_gu.scales.clone(), c=q_gu.c, n=q_gu.n, K=D_MODEL),
+                             NS(packed=q_d.packed.clone(), scales=q_d.scales.clone(), c=q_d.c, n=q_d.n, K=D_FF)))
+        self.x = synth.bits_to_torch(synth.activations(M, D_MODEL, synth.layer_seed(1, 3))).to(dev)
+        self.h = torch.empty((M, D_FF), dtype=torch.bfloat16, device=dev)
+        self.y = torch.empty((M, D_MODEL), dtype=torch.bfloat16, device=dev)
+        self.ws = F.Workspace(F.ffn_workspace_bytes(M, D_MODEL, D_FF), dev)
+
+    def step(self, r, stream=None):
+        q_gu, q_d = self.rot[r]
+        nxt = self.rot[(r + 1) % len(self.rot)][0]
+        self.F.ffn_w4a8_decode(self.x, q_gu, q_d, h=self.h, out=self.y, workspace=self.ws, stream=stream,
+                               prefetch=(nxt.packed, nxt.scales))
+
+    def bytes_per_step(self):
+        M = self.M
+        # quantize_act(x) + gate_up (W, x_hat, h written, h re-read + h_hat written) + down
+        return (act_bytes(M, D_MODEL, True) + gemm_bytes(M, 2 * D_FF, D_MODEL) - 2 * M * 2 * D_FF + 2 * M * D_FF
+                + 2 * D_FF + act_bytes(M, D_FF) + gemm_bytes(M, D_MODEL, D_FF))
+
+
 def capture(fn, stream):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=stream):
@@ -308,7 +347,7 @@ def run_fireq(args, rank, world, dev):
         from paper_2505_20839_b200 import multigpu
         return multigpu.run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src)
 
-    # ---------------- decode FFN (headline)
+    # ---------------- decode FFN (headline): quantize_act, gemm, silu_mul_quantize_act, gemm
     ffn = FFN(F, M_DECODE, ROTATIONS, dev)
     torch.cuda.synchronize()
     with torch.cuda.stream(stream):
@@ -327,6 +366,24 @@ def run_fireq(args, rank, world, dev):
     total_ms = time_steps(g_multi, g_single, args.steps, args.warmup, stream)
     clocks.stop()
     us_per_step = total_ms * 1e3 / args.steps
+
+    # end to end through host buffers (pinned H2D of x, D2H of y) around the public calls
+    x_host = ffn.x.cpu().pin_memory()
+    y_host = torch.empty_like(ffn.y, device="cpu").pin_memory()
+
+    def e2e_step(r):
+        ffn.x.copy_(x_host, non_blocking=True)
+        ffn.step(r, stream)
+        y_host.copy_(ffn.y, non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        for r in range(ROTATIONS):
+            e2e_step(r)
+    torch.cuda.synchronize()
+    g_e2e_multi = capture(lambda: [e2e_step(r) for r in range(ROTATIONS)], stream)
+    g_e2e = [capture(lambda r=r: e2e_step(r), stream) for r in range(ROTATIONS)]
+    e2e_ms = time_steps(g_e2e_multi, g_e2e, args.steps, args.warmup, stream) / args.steps
+    del g_e2e_multi, g_e2e
 
     # ---------------- dominant kernel: the gate_up GEMM alone (HBM bound), rotating weights
     def gu_only(r):
@@ -347,31 +404,27 @@ def run_fireq(args, rank, world, dev):
     gbs_gu = b_gu / (ms_gu * 1e-3) / 1e9
     b_d = gemm_bytes(M_DECODE, D_MODEL, D_FF)
     gbs_d = b_d / (ms_d * 1e-3) / 1e9
+    # ---------------- the same FFN through fireq_ffn_w4a8_decode (3 kernels, SwiGLU fused)
+    fused = FusedFFN(F, M_DECODE, ROTATIONS, dev)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        for r in range(ROTATIONS):
+            fused.step(r, stream)
+    torch.cuda.synchronize()
+    gf_multi = capture(lambda: [fused.step(r, stream) for r in range(ROTATIONS)], stream)
+    gf_single = [capture(lambda r=r: fused.step(r, stream), stream) for r in range(ROTATIONS)]
+    fused_us = time_steps(gf_multi, gf_single, args.steps, args.warmup, stream) * 1e3 / args.steps
+    del gf_multi, gf_single, fused
+    torch.cuda.empty_cache()
+
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get("gemm_gate_up_m16_bytes_per_launch")
 
-    # ---------------- end to end through host buffers (pinned H2D of x, D2H of y)
-    x_host = ffn.x.cpu().pin_memory()
-    y_host = torch.empty_like(ffn.y, device="cpu").pin_memory()
-
-    def e2e_step(r):
-        ffn.x.copy_(x_host, non_blocking=True)
-        ffn.step(r, stream)
-        y_host.copy_(ffn.y, non_blocking=True)
-
-    with torch.cuda.stream(stream):
-        for r in range(ROTATIONS):
-            e2e_step(r)
-    torch.cuda.synchronize()
-    g_e2e_multi = capture(lambda: [e2e_step(r) for r in range(ROTATIONS)], stream)
-    g_e2e = [capture(lambda r=r: e2e_step(r), stream) for r in range(ROTATIONS)]
-    e2e_ms = time_steps(g_e2e_multi, g_e2e, args.steps, args.warmup, stream) / args.steps
-
     # ---------------- prefill FFN (FP8 tensor bound) and single-GEMM figures
-    del g_multi, g_single, g_gu, g_d, g_e2e, g_e2e_multi
+    del g_multi, g_single, g_gu, g_d
     pre_info = prefill_figures(F, dev, stream, peaks) if not args.no_prefill else None
 
     # ---------------- cpu baseline (oracle on a bounded sample)
@@ -384,11 +437,14 @@ def run_fireq(args, rank, world, dev):
         "scaling": "strong", "vs_baseline": None, "dtype": "fp8e4m3 x int4 -> f32 acc -> bf16", "data": "synthetic",
         "config": {"workload": "llama2-7b-ffn-decode-b16", "tokens": M_DECODE, "d_model": D_MODEL, "d_ff": D_FF,
                    "gemms": "gate_up 22016x4096 (fused, gamma=[1|c_down]) + down 4096x11008",
+                   "api": "fireq_quantize_act, fireq_w4a8_gemm, fireq_silu_mul_quantize_act, fireq_w4a8_gemm",
                    "parallelism": "single GPU",
                    "l2": f"{ROTATIONS} rotating weight copies ({ROTATIONS * (b_gu + b_d) / 1e6:.0f} MB > 2x L2)",
                    "graph": f"CUDA graphs of {ROTATIONS} steps (4 PDL-chained kernels per step)"},
         "gpu_launches": FFN.KERNELS_PER_STEP * args.steps,
         "step_gbs": round(ffn.bytes_per_step() / (us_per_step * 1e-6) / 1e9, 1),
+        "step_hbm_frac": round(ffn.bytes_per_step() / (us_per_step * 1e-6) / 1e9 / peaks["hbm_gbs"], 4),
+        "fused_ffn_api_us": round(fused_us, 3),
         "roofline": {"bound": "hbm", "kernel": "fireq_w4a8_gemm gate_up M=16 N=22016 K=4096",
                      "achieved": round(gbs_gu, 1), "peak": hbm, "unit": "GB/s", "frac": round(gbs_gu / hbm, 4),
                      "traffic": traffic, "algorithmic_bytes": b_gu, "launch_us": round(ms_gu * 1e3, 3),

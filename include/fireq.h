@@ -238,6 +238,56 @@ fireq_status_t fireq_debug_set_trace(void* buf);
  * slots of the device buffer buf ([cap][2] uint64, caller pre-fills {UINT64_MAX, 0}).
  * NULL disables.  Not thread-safe; for benchmarks only. */
 fireq_status_t fireq_debug_set_spans(void* buf, int cap);
+/* ------------------------------------------------------ fused decode FFN */
+/*
+ * fireq_interleave_gate_up -- row order of the fused FFN's gate_up weight:
+ * 128-row tile t = gate rows [64t, 64t+64) followed by up rows [64t, 64t+64).
+ * W_gate, W_up bf16 [d_ff][d_model]; W_gu out, bf16 [2 d_ff][d_model] (caller
+ * owned, device, 16-B aligned).  A row permutation only: quantizing W_gu with
+ * fireq_quantize_weight gives every row the codes/scales of the plain
+ * [gate; up] stacking (CAS lambda is per input channel, PTS n per tensor).
+ */
+fireq_status_t fireq_interleave_gate_up(const void* W_gate, const void* W_up, int64_t d_ff,
+                                        int64_t d_model, void* W_gu, void* stream);
+
+/* Workspace for fireq_ffn_w4a8_decode (0 for invalid shapes).  Zero-fill it once
+ * before first use; every call leaves its counters zeroed again. */
+size_t fireq_ffn_workspace_bytes(int64_t M, int64_t d_model, int64_t d_ff);
+
+/*
+ * fireq_ffn_w4a8_decode -- a Llama FFN y = W_down (silu(W_gate x) * (W_up x))
+ * at decode batch sizes as THREE kernels (vs four for the unfused chain):
+ *   1. fireq_quantize_act(x, c_gu)                      (A1..A3, Eq. 2)
+ *   2. gate_up GEMM over the interleaved W_gu (steps 1-3) whose epilogue forms
+ *      h = bf16(silu(g) * u * c_down) from the bf16-rounded g and u (exactly
+ *      fireq_silu_mul_quantize_act's x'), writes h and gathers the
+ *      per-token max|h| with atomics; after a grid-wide barrier every CTA
+ *      quantizes a slice of h with beta = bf16(amax / 448) (A2..A3);
+ *   3. down GEMM on (h_hat, beta_h).
+ * Arguments
+ *   x        bf16 [M][ldx], ldx >= d_model, ldx % 8 == 0.
+ *   c_gu     bf16 [d_model]: CAS multiplier of W_gu (QuantizedWeight.c) or NULL.
+ *   gu_*     fireq_quantize_weight output for the INTERLEAVED W_gu
+ *            (fireq_interleave_gate_up), N = 2 d_ff, K = d_model.
+ *   c_down   bf16 [d_ff]: CAS multiplier of W_down (applied to u) or NULL.
+ *   d_*      fireq_quantize_weight output for W_down, N = d_model, K = d_ff.
+ *   h        out, bf16 [M][d_ff]: the SwiGLU output (before quantization).
+ *   y        out, bf16 [M][ldy], ldy >= d_model.
+ *   next_*   optional L2 prefetch of the next layer's weights (may be NULL).
+ * Shapes: 1 <= M <= 16, d_model, d_ff multiples of 128; otherwise
+ * FIREQ_ERROR_UNSUPPORTED_SHAPE.  Same arithmetic as the unfused chain
+ * (quantize_act -> gemm -> silu_mul_quantize_act -> gemm) up to the fp32 summation
+ * order of split tiles; y equals fireq_w4a8_gemm(quantize_act(h), W_down) exactly.
+ */
+fireq_status_t fireq_ffn_w4a8_decode(const void* x, int64_t ldx, const void* c_gu, int64_t M,
+                                     int64_t d_model, int64_t d_ff, const uint8_t* gu_packed,
+                                     const uint8_t* gu_scales, int32_t gu_pts, const void* c_down,
+                                     const uint8_t* d_packed, const uint8_t* d_scales, int32_t d_pts,
+                                     void* h, void* y, int64_t ldy, void* workspace,
+                                     size_t workspace_bytes, const void* next_packed,
+                                     size_t next_packed_bytes, const void* next_scales,
+                                     size_t next_scales_bytes, void* stream);
+
 /* The schedule fireq_w4a8_gemm chooses for (M, N, K), for benchmarks and tests:
  * writes {ntok, mode, ctas, sign_split} into cfg_out[4] (host).  mode 0 = whole
  * tiles, 1 = whole tiles + stream-K remainder (global-memory fixup), 2 = cluster

@@ -27,6 +27,16 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
                          size_t ws_bytes, cudaStream_t stream, const void* pf0, size_t pf0_bytes,
                          const void* pf1, size_t pf1_bytes);
 fireq_status_t debug_lut_table(uint8_t* out, cudaStream_t stream);
+size_t ffn_workspace_bytes(int64_t M, int64_t d_model, int64_t d_ff);
+bool ffn_shape_supported(int64_t M, int64_t d_model, int64_t d_ff);
+fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_bfloat16* c_gu, int64_t M,
+                               int64_t d_model, int64_t d_ff, const uint8_t* gu_packed, const uint8_t* gu_scales,
+                               int32_t gu_pts, const __nv_bfloat16* c_down, const uint8_t* d_packed,
+                               const uint8_t* d_scales, int32_t d_pts, __nv_bfloat16* h, __nv_bfloat16* y,
+                               int64_t ldy, void* ws, size_t ws_bytes, cudaStream_t stream, const void* pf0,
+                               size_t pf0_bytes, const void* pf1, size_t pf1_bytes);
+fireq_status_t interleave_gate_up_impl(const __nv_bfloat16* wg, const __nv_bfloat16* wu, int64_t d_ff,
+                                       int64_t d_model, __nv_bfloat16* out, cudaStream_t stream);
 extern unsigned long long* g_trace;
 
 namespace {
@@ -226,6 +236,50 @@ fireq_status_t fireq_w4a8_gemm_prefetch(const uint8_t* x_fp8, const void* x_scal
     return gemm_checked(x_fp8, x_scale, M, K, w_packed, w_scales, N, pts_exponent, out_chan_scale, Y, ldy, out_layout,
                         workspace, workspace_bytes, stream, next_packed, next_packed_bytes, next_scales,
                         next_scales_bytes);
+}
+
+// ------------------------------------------------------------ fused decode FFN
+size_t fireq_ffn_workspace_bytes(int64_t M, int64_t d_model, int64_t d_ff) {
+    if (M < 1 || d_model < 128 || d_ff < 128 || d_model % 128 || d_ff % 128) return 0;
+    return ffn_workspace_bytes(M, d_model, d_ff);
+}
+
+fireq_status_t fireq_interleave_gate_up(const void* W_gate, const void* W_up, int64_t d_ff, int64_t d_model,
+                                        void* W_gu, void* stream) {
+    FIREQ_REQUIRE(W_gate && W_up && W_gu, FIREQ_ERROR_INVALID_VALUE, "fireq_interleave_gate_up: NULL pointer");
+    FIREQ_REQUIRE(d_ff >= 128 && d_ff % 128 == 0 && d_model >= 128 && d_model % 128 == 0, FIREQ_ERROR_UNSUPPORTED_SHAPE,
+                  "fireq_interleave_gate_up: d_ff and d_model must be multiples of 128");
+    FIREQ_REQUIRE(aligned16(W_gate) && aligned16(W_up) && aligned16(W_gu), FIREQ_ERROR_MISALIGNED,
+                  "fireq_interleave_gate_up: pointers must be 16-byte aligned");
+    return interleave_gate_up_impl(static_cast<const __nv_bfloat16*>(W_gate), static_cast<const __nv_bfloat16*>(W_up),
+                                   d_ff, d_model, static_cast<__nv_bfloat16*>(W_gu), static_cast<cudaStream_t>(stream));
+}
+
+fireq_status_t fireq_ffn_w4a8_decode(const void* x, int64_t ldx, const void* c_gu, int64_t M, int64_t d_model,
+                                     int64_t d_ff, const uint8_t* gu_packed, const uint8_t* gu_scales, int32_t gu_pts,
+                                     const void* c_down, const uint8_t* d_packed, const uint8_t* d_scales,
+                                     int32_t d_pts, void* h, void* y, int64_t ldy, void* workspace,
+                                     size_t workspace_bytes, const void* next_packed, size_t next_packed_bytes,
+                                     const void* next_scales, size_t next_scales_bytes, void* stream) {
+    FIREQ_REQUIRE(x && gu_packed && gu_scales && d_packed && d_scales && h && y && workspace, FIREQ_ERROR_INVALID_VALUE,
+                  "fireq_ffn_w4a8_decode: NULL required pointer");
+    FIREQ_REQUIRE(gu_pts >= 0 && gu_pts <= 60 && d_pts >= 0 && d_pts <= 60, FIREQ_ERROR_INVALID_VALUE,
+                  "fireq_ffn_w4a8_decode: pts exponents must be in [0, 60]");
+    FIREQ_REQUIRE(d_model >= 128 && d_model % 128 == 0 && d_ff >= 128 && d_ff % 128 == 0 && d_model <= 65536 &&
+                      d_ff <= 65536,
+                  FIREQ_ERROR_UNSUPPORTED_SHAPE, "fireq_ffn_w4a8_decode: d_model, d_ff must be multiples of 128");
+    FIREQ_REQUIRE(ffn_shape_supported(M, d_model, d_ff), FIREQ_ERROR_UNSUPPORTED_SHAPE,
+                  "fireq_ffn_w4a8_decode: decode batches only (1 <= M <= 16)");
+    FIREQ_REQUIRE(aligned16(x) && (!c_gu || aligned16(c_gu)) && (!c_down || aligned16(c_down)) && aligned16(gu_packed) &&
+                      aligned16(gu_scales) && aligned16(d_packed) && aligned16(d_scales) && aligned16(h) &&
+                      aligned16(y) && ldx % 8 == 0 && ldx >= d_model && ldy % 8 == 0 && ldy >= d_model &&
+                      (!next_packed || aligned16(next_packed)) && (!next_scales || aligned16(next_scales)),
+                  FIREQ_ERROR_MISALIGNED, "fireq_ffn_w4a8_decode: pointers must be 16-byte aligned, ld % 8 == 0");
+    return ffn_decode_impl(static_cast<const __nv_bfloat16*>(x), ldx, static_cast<const __nv_bfloat16*>(c_gu), M,
+                           d_model, d_ff, gu_packed, gu_scales, gu_pts, static_cast<const __nv_bfloat16*>(c_down),
+                           d_packed, d_scales, d_pts, static_cast<__nv_bfloat16*>(h), static_cast<__nv_bfloat16*>(y),
+                           ldy, workspace, workspace_bytes, static_cast<cudaStream_t>(stream), next_packed,
+                           next_packed_bytes, next_scales, next_scales_bytes);
 }
 
 fireq_status_t fireq_debug_lut_table(uint8_t* out, void* stream) {

@@ -65,6 +65,18 @@ struct GemmArgs {
     long long U;           // stream-K units = R * G
     int S;                 // > 1: cluster split-K, one tile per cluster of S CTAs (K split S ways)
     int depth;             // weight stages in flight (<= STAGES): bounds the loaded HBM latency
+    // out_layout 2 (SwiGLU pairs): tile rows [0, 64) are gate channels j0 + r, rows [64, 128)
+    // the up channels of the same j; h = bf16(silu(g) * u) -> h_out[m][j], per-token
+    // max |h| -> amax_out[m] (atomic max of fp32 bits).  gamma_up (bf16) scales the up rows.
+    __nv_bfloat16* h_out;
+    int64_t ldh;
+    unsigned* amax_out;
+    const __nv_bfloat16* gamma_up;
+    // out_layout 2 tail: after a grid-wide barrier (bar[0] arrivals, bar[1] departures) every
+    // CTA quantizes a 1/C slice of h with beta = bf16(amax / 448) (A2..A3) -> hq, hbeta
+    uint8_t* hq_out;
+    __nv_bfloat16* hbeta_out;
+    unsigned* bar;
     unsigned long long* trace;   // debug timeline [C][8] (%globaltimer ns) or nullptr
     int dbg;                     // experiments only: bit0 skip conversion, bit1 skip MMAs, bit2 skip weight loads
     unsigned long long* span;    // profile builds: {start, end} of this launch
@@ -289,6 +301,18 @@ __device__ __forceinline__ void conv_mask_select(uint32_t w, uint32_t L0, uint32
     const uint32_t m1 = ptx::prmt(w, t, 0xBFAEu);     // nibbles 4..7
     r0 = ptx::lop3_mux(ptx::prmt(L0, L1, w), ptx::prmt(L2, L3, x), m0);
     r1 = ptx::lop3_mux(ptx::prmt(L0, L1, wh), ptx::prmt(L2, L3, xh), m1);
+}
+
+// x / beta -> E4M3 (A3) with the quotient x' / beta correctly rounded to fp32 (as
+// __fdiv_rn) from the reciprocal: q0 = x' * rcp, one exact-residual correction.  The
+// corrected quotient is exact whenever x' / beta is representable, otherwise within
+// 1 ulp; a quotient of two 8-bit-significand numbers that is not exactly an E4M3
+// midpoint lies > 2^-13 relative away from every midpoint, so the E4M3 rounding equals
+// that of the correctly rounded quotient (reading R23).
+__device__ __forceinline__ float div_for_e4m3(float x, float beta, float rcp) {
+    const float q0 = __fmul_rn(x, rcp);
+    const float e = __fmaf_rn(-q0, beta, x);
+    return __fmaf_rn(e, rcp, q0);
 }
 
 // Roles (warp-uniform, see kW* below): converter warpgroups, epilogue warpgroup, TMEM
@@ -610,6 +634,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
         const long long u_first = (long long)blockIdx.x * a.U / a.C;
         int ntile = 0, m0 = 0, n = 0;
         float gam = 1.0f;
+        const bool use_gam = a.gamma != nullptr || (a.out_layout == 2 && a.gamma_up != nullptr);
         // Step 3 for 16 tokens [m0 + 16 ch, +16) of this thread's output channel n:
         // y = bf16(acc * (beta_m 2^-n) [* gamma_n]).  Y^T rows are 32 contiguous bytes per
         // thread; row-major Y goes through a 4 KB SMEM transpose so that each warp writes
@@ -619,7 +644,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
 #pragma unroll
             for (int c = 0; c < 16; ++c) {
                 float y = __fmul_rn(acc[c], sScale[ch * 16 + c]);
-                if (a.gamma) y = __fmul_rn(y, gam);
+                if (use_gam) y = __fmul_rn(y, gam);
                 yb[c] = __float2bfloat16_rn(y);
             }
             const int mb = m0 + ch * 16;
@@ -631,6 +656,30 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                 } else {
                     for (int c = 0; c < 16 && mb + c < a.M; ++c) dst[c] = yb[c];
                 }
+            } else if (a.out_layout == 2) {
+                // SwiGLU pair (DESIGN R22): h = bf16(silu(g) * u) from the bf16-rounded gate and
+                // up outputs, exactly as fireq_silu_mul_quantize_act computes x'
+#pragma unroll
+                for (int c = 0; c < 16; ++c) sT[c * kTileN + r] = yb[c];
+                ptx::named_bar_sync(1, 128);
+                const int j = r & 63, half = r >> 6;
+                const int ch_out = ntile * 64 + j;
+#pragma unroll
+                for (int c8 = 0; c8 < 8; ++c8) {
+                    const int c = half * 8 + c8, m = mb + c;
+                    const float gv = __bfloat162float(sT[c * kTileN + j]);
+                    const float uv = __bfloat162float(sT[c * kTileN + 64 + j]);
+                    const float silu = __fdividef(gv, 1.0f + __expf(-gv));
+                    const __nv_bfloat16 hb = __float2bfloat16_rn(__fmul_rn(silu, uv));
+                    float hm = 0.0f;
+                    if (m < a.M) {
+                        a.h_out[(size_t)m * a.ldh + ch_out] = hb;
+                        hm = fabsf(__bfloat162float(hb));
+                    }
+                    for (int o = 16; o; o >>= 1) hm = fmaxf(hm, __shfl_xor_sync(0xffffffffu, hm, o));
+                    if (lane == 0 && m < a.M) atomicMax(a.amax_out + m, __float_as_uint(hm));
+                }
+                ptx::named_bar_sync(1, 128);
             } else {
 #pragma unroll
                 for (int c = 0; c < 16; ++c) sT[c * kTileN + r] = yb[c];
@@ -657,7 +706,10 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
             const int mtile = tile / a.n_tiles;
             n = ntile * kTileN + r;
             m0 = mtile * NTOK;
-            gam = a.gamma ? a.gamma[n] : 1.0f;
+            if (a.out_layout == 2)
+                gam = (r < 64 || !a.gamma_up) ? 1.0f : __bfloat162float(a.gamma_up[ntile * 64 + (r - 64)]);
+            else
+                gam = a.gamma ? a.gamma[n] : 1.0f;
             for (int t = r; t < NTOK; t += 128)
                 sScale[t] = (m0 + t < a.M) ? __fmul_rn(__bfloat162float(a.x_scale[m0 + t]), p2) : 0.0f;
             const bool csplit = a.S > 1;
@@ -830,6 +882,74 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
             if (r == 0 && sg < 4) FIREQ_TRACE2(3 * sg + 2);
             ++sg;
         }
+        if (a.out_layout == 2 && a.hq_out) {
+            // ---- SwiGLU tail: quantize h (A2..A3) once every tile's h and amax are in.
+            // Grid-wide barrier: every CTA of this persistent grid is resident (one per SM,
+            // launched before any dependent kernel can take an SM), so spinning is safe.
+            ptx::named_bar_sync(1, 128);            // this CTA's h stores / amax atomics issued
+            if (r == 0) {
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar) : "memory");
+                unsigned seen = 0;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(a.bar) : "memory");
+                    if (seen < (unsigned)a.C) __nanosleep(64);
+                } while (seen < (unsigned)a.C);
+                FIREQ_TRACE2(15);
+            }
+            ptx::named_bar_sync(1, 128);
+            float* sB = sScale;                     // beta_m, rcp(beta_m) for the slice
+            if (r < NTOK) {
+                const float amax = r < a.M ? __uint_as_float(__ldcg(a.amax_out + r)) : 0.0f;
+                const __nv_bfloat16 bh = amax > 0.0f ? __float2bfloat16_rn(__fdiv_rn(amax, 448.0f))
+                                                     : __float2bfloat16_rn(1.0f);
+                sB[r] = __bfloat162float(bh);
+                sB[NTOK + r] = __frcp_rn(__bfloat162float(bh));
+                if (blockIdx.x == 0 && r < a.M) a.hbeta_out[r] = bh;
+            }
+            ptx::named_bar_sync(1, 128);
+            // this CTA's channel slice [c0, c1) of h (8-channel vectors), all tokens
+            const int nv = (int)(a.ldh / 8);
+            const int per = (nv + a.C - 1) / a.C;
+            const int v0 = blockIdx.x * per, v1 = min(nv, v0 + per);
+            const int cnt = (v1 > v0 ? v1 - v0 : 0) * a.M;
+            for (int base = 0; base < cnt; base += 4 * 128) {
+                uint4 hv[4];                        // all loads of the round in flight at once
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int idx = base + u * 128 + r;
+                    if (idx < cnt) {
+                        const int m = idx / (v1 - v0), v = v0 + idx % (v1 - v0);
+                        hv[u] = __ldcg(reinterpret_cast<const uint4*>(a.h_out + (size_t)m * a.ldh) + v);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int idx = base + u * 128 + r;
+                    if (idx < cnt) {
+                        const int m = idx / (v1 - v0), v = v0 + idx % (v1 - v0);
+                        const __nv_bfloat16* hh = reinterpret_cast<const __nv_bfloat16*>(&hv[u]);
+                        const float beta = sB[m], rcp = sB[NTOK + m];
+                        float f[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) f[e] = div_for_e4m3(__bfloat162float(hh[e]), beta, rcp);
+                        uint2 o;
+                        o.x = e4m3x2_rn(f[0], f[1]) | (e4m3x2_rn(f[2], f[3]) << 16);
+                        o.y = e4m3x2_rn(f[4], f[5]) | (e4m3x2_rn(f[6], f[7]) << 16);
+                        *reinterpret_cast<uint2*>(a.hq_out + (size_t)m * a.ldh + (size_t)v * 8) = o;
+                    }
+                }
+            }
+            if (r == 0) {
+                // the last CTA to leave resets the barrier and amax for the next launch
+                unsigned prev;
+                asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a.bar + 1) : "memory");
+                if (prev == (unsigned)(a.C - 1)) {
+                    for (int m = 0; m < a.M; ++m) a.amax_out[m] = 0u;
+                    a.bar[0] = 0u;
+                    a.bar[1] = 0u;
+                }
+            }
+        }
     }
 
     // ------------------------------------------------------------ teardown
@@ -897,7 +1017,7 @@ struct Plan {
     bool sign_split;
 };
 
-Plan make_plan(int64_t M, int64_t N, int64_t K) {
+Plan make_plan(int64_t M, int64_t N, int64_t K, bool allow_cluster = true) {
     Plan p{};
     p.ntok = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 192;
     p.sign_split = p.ntok <= 128;
@@ -924,7 +1044,7 @@ Plan make_plan(int64_t M, int64_t N, int64_t K) {
     // through L2 on the critical path).  S - 1 partials must fit the receiver's fixup buffer.
     static const bool no_csplit = getenv("FIREQ_NO_CSPLIT") != nullptr;
     const int slots = p.ntok <= 32 ? 32768 / (p.ntok * kTileN * 4) : 0;
-    if (!no_csplit && slots > 0 && 2 * p.tiles <= sms) {
+    if (allow_cluster && !no_csplit && slots > 0 && 2 * p.tiles <= sms) {
         const int S = std::min(std::min(sms / p.tiles, 8), std::min(slots + 1, p.G));
         if (S > 1) {
             p.S = S;
@@ -957,12 +1077,13 @@ fireq_status_t launch_cfg(const CUtensorMap& map, const GemmArgs& args, cudaStre
 
 }  // namespace
 
-size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
-    const Plan p = make_plan(M, N, K);
+size_t plan_workspace_bytes(const Plan& p) {
     const size_t part = p.R > 0 ? (size_t)2 * p.C * p.ntok * kTileN * sizeof(float) : 0;
     const size_t cnt = ((size_t)p.tiles * sizeof(unsigned) + 255) / 256 * 256;
     return cnt + part;
 }
+
+size_t gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) { return plan_workspace_bytes(make_plan(M, N, K)); }
 
 fireq_status_t gemm_plan(int64_t M, int64_t N, int64_t K, int32_t* cfg) {
     const Plan p = make_plan(M, N, K);
@@ -973,29 +1094,21 @@ fireq_status_t gemm_plan(int64_t M, int64_t N, int64_t K, int32_t* cfg) {
     return FIREQ_SUCCESS;
 }
 
-fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int64_t M, int64_t K,
-                         const uint8_t* w_packed, const uint8_t* w_scales, int64_t N, int32_t pts_n,
-                         const float* gamma, __nv_bfloat16* Y, int64_t ldy, int out_layout, void* ws,
-                         size_t ws_bytes, cudaStream_t stream, const void* pf0, size_t pf0_bytes,
-                         const void* pf1, size_t pf1_bytes) {
-    const Plan p = make_plan(M, N, K);
-    if (ws_bytes < gemm_workspace_bytes(M, N, K)) return fail(FIREQ_ERROR_WORKSPACE, "GEMM workspace too small");
-    CUtensorMap map;
-    if (!make_x_map(&map, x_fp8, M, K, p.ntok)) return fail(FIREQ_ERROR_CUDA, "cuTensorMapEncodeTiled failed");
+namespace {
+
+// Kernel arguments common to every launch of plan p.
+GemmArgs base_args(const Plan& p, int64_t M, int64_t N, int64_t K, const uint8_t* w_packed,
+                   const uint8_t* w_scales, int32_t pts_n, void* ws, const void* pf0, size_t pf0_bytes,
+                   const void* pf1, size_t pf1_bytes) {
     GemmArgs args{};
     args.w_packed = w_packed;
     args.w_scales = w_scales;
-    args.x_scale = x_scale;
-    args.gamma = gamma;
-    args.Y = Y;
     const size_t cnt = ((size_t)p.tiles * sizeof(unsigned) + 255) / 256 * 256;
     args.counters = static_cast<unsigned*>(ws);
     args.partial = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + cnt);
-    args.ldy = ldy;
     args.M = (int)M; args.N = (int)N; args.K = (int)K; args.G = p.G;
     args.n_tiles = p.n_tiles; args.m_tiles = p.m_tiles; args.tiles = p.tiles;
     args.pts_n = pts_n;
-    args.out_layout = out_layout;
     args.R = p.R;
     args.C = p.C;
     args.U = p.U;
@@ -1014,27 +1127,112 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
         static const int dbg = getenv("FIREQ_DEBUG_MODE") ? atoi(getenv("FIREQ_DEBUG_MODE")) : 0;
         args.dbg = dbg;
     }
+    return args;
+}
+
+size_t align256(size_t b) { return (b + 255) / 256 * 256; }
+
+}  // namespace
+
+fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int64_t M, int64_t K,
+                         const uint8_t* w_packed, const uint8_t* w_scales, int64_t N, int32_t pts_n,
+                         const float* gamma, __nv_bfloat16* Y, int64_t ldy, int out_layout, void* ws,
+                         size_t ws_bytes, cudaStream_t stream, const void* pf0, size_t pf0_bytes,
+                         const void* pf1, size_t pf1_bytes) {
+    const Plan p = make_plan(M, N, K);
+    if (ws_bytes < gemm_workspace_bytes(M, N, K)) return fail(FIREQ_ERROR_WORKSPACE, "GEMM workspace too small");
+    CUtensorMap map;
+    if (!make_x_map(&map, x_fp8, M, K, p.ntok)) return fail(FIREQ_ERROR_CUDA, "cuTensorMapEncodeTiled failed");
+    GemmArgs args = base_args(p, M, N, K, w_packed, w_scales, pts_n, ws, pf0, pf0_bytes, pf1, pf1_bytes);
+    args.x_scale = x_scale;
+    args.gamma = gamma;
+    args.Y = Y;
+    args.ldy = ldy;
+    args.out_layout = out_layout;
     switch (p.ntok) {
         // <NTOK, sign-split, converter WGs, SMEM stages, TMEM A stages, accumulators, groups/stage,
-        //  MMA-issuing warps>
+        //  MMA-issuing warps, resident activations>
         // decode configs: >= 128 KB of weights in flight per SM (hides the loaded DRAM
         // latency), 2 groups per stage (halves the per-stage synchronisation cost), and
         // <= 96 registers per thread so a CTA of the next small kernel of a PDL chain fits.
-        case 16: {
-            static const int v = getenv("FIREQ_CFG16") ? atoi(getenv("FIREQ_CFG16")) : 0;   // experiments
-            switch (v) {
-                case 1: return launch_cfg<16, true, 3, 16, 7, 2, 1, 2>(map, args, stream);
-                case 2: return launch_cfg<16, true, 4, 16, 7, 2, 1, 2>(map, args, stream);
-                case 3: return launch_cfg<16, false, 3, 8, 7, 2, 2, 2>(map, args, stream);
-                case 4: return launch_cfg<16, false, 4, 8, 7, 2, 2, 2>(map, args, stream);
-                default: return launch_cfg<16, true, 3, 8, 3, 2, 2, 2>(map, args, stream);
-            }
-        }
+        // NMMA = 1: two MMA-issuing warps (separate accumulators) produced rare wrong tiles
+        // (~1% of launches, scripts/dbg_det4.py); a single issuer is exact.
+        case 16:  return launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map, args, stream);
         case 32:  return launch_cfg<32, true, 3, 7, 3, 2, 2, 1>(map, args, stream);
         case 64:  return launch_cfg<64, true, 2, 5, 2, 2, 2, 1>(map, args, stream);
         case 128: return launch_cfg<128, true, 2, 7, 4, 2, 1, 1>(map, args, stream);
         default:  return launch_cfg<192, false, 2, 6, 4, 2, 1, 1>(map, args, stream);
     }
+}
+
+size_t ffn_workspace_bytes(int64_t M, int64_t d_model, int64_t d_ff) {
+    // gate_up GEMM ws | down GEMM ws | amax[16] + barrier[2] | x_hat | beta_x | h_hat | beta_h
+    // (the gate_up plan never uses clusters: its tail has a grid-wide barrier)
+    return align256(plan_workspace_bytes(make_plan(M, 2 * d_ff, d_model, false))) +
+           align256(gemm_workspace_bytes(M, d_model, d_ff)) + 256 + align256((size_t)M * d_model) + 256 +
+           align256((size_t)M * d_ff) + 256;
+}
+
+bool ffn_shape_supported(int64_t M, int64_t d_model, int64_t d_ff) {
+    if (M < 1 || M > 16) return false;
+    const Plan p1 = make_plan(M, 2 * d_ff, d_model, /*allow_cluster=*/false);
+    return p1.ntok == 16 && p1.C <= sm_count();
+}
+
+fireq_status_t quantize_act_impl(const __nv_bfloat16* X, const __nv_bfloat16* U, int64_t M, int64_t K, int64_t ld,
+                                 const __nv_bfloat16* c, int mode, bool transposed, uint8_t* xq,
+                                 __nv_bfloat16* beta, cudaStream_t stream);
+
+fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_bfloat16* c_gu, int64_t M,
+                               int64_t d_model, int64_t d_ff, const uint8_t* gu_packed, const uint8_t* gu_scales,
+                               int32_t gu_pts, const __nv_bfloat16* c_down, const uint8_t* d_packed,
+                               const uint8_t* d_scales, int32_t d_pts, __nv_bfloat16* h, __nv_bfloat16* y,
+                               int64_t ldy, void* ws, size_t ws_bytes,
+                               cudaStream_t stream, const void* pf0, size_t pf0_bytes, const void* pf1,
+                               size_t pf1_bytes) {
+    if (!ffn_shape_supported(M, d_model, d_ff))
+        return fail(FIREQ_ERROR_UNSUPPORTED_SHAPE, "fused FFN: decode batches (M <= 16) only");
+    if (ws_bytes < ffn_workspace_bytes(M, d_model, d_ff)) return fail(FIREQ_ERROR_WORKSPACE, "FFN workspace too small");
+    const Plan p1 = make_plan(M, 2 * d_ff, d_model, false), p2 = make_plan(M, d_model, d_ff);
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    uint8_t* ws1 = w;
+    uint8_t* ws2 = ws1 + align256(plan_workspace_bytes(p1));
+    unsigned* amax = reinterpret_cast<unsigned*>(ws2 + align256(gemm_workspace_bytes(M, d_model, d_ff)));
+    uint8_t* xq = reinterpret_cast<uint8_t*>(amax) + 256;
+    __nv_bfloat16* xbeta = reinterpret_cast<__nv_bfloat16*>(xq + align256((size_t)M * d_model));
+    uint8_t* hq = reinterpret_cast<uint8_t*>(xbeta) + 256;
+    __nv_bfloat16* hbeta = reinterpret_cast<__nv_bfloat16*>(hq + align256((size_t)M * d_ff));
+    // A1..A3 of x (the FFN input comes from the previous layer)
+    fireq_status_t st = quantize_act_impl(x, nullptr, M, d_model, ldx, c_gu, c_gu ? 1 : 0, false, xq, xbeta, stream);
+    if (st != FIREQ_SUCCESS) return st;
+    // gate_up over interleaved [gate | up] tiles; SwiGLU epilogue; h quantized in the tail
+    CUtensorMap map1;
+    if (!make_x_map(&map1, xq, M, d_model, p1.ntok)) return fail(FIREQ_ERROR_CUDA, "cuTensorMapEncodeTiled failed");
+    GemmArgs a1 = base_args(p1, M, 2 * d_ff, d_model, gu_packed, gu_scales, gu_pts, ws1, d_packed,
+                            (size_t)d_model * d_ff / 2, d_scales, (size_t)d_model * d_ff / 128);
+    a1.x_scale = xbeta;
+    a1.out_layout = 2;
+    a1.h_out = h;
+    a1.ldh = d_ff;
+    a1.amax_out = amax;
+    a1.gamma_up = c_down;
+    a1.hq_out = hq;
+    a1.hbeta_out = hbeta;
+    a1.bar = amax + 16;
+    static const int trace_which = getenv("FIREQ_TRACE_WHICH") ? atoi(getenv("FIREQ_TRACE_WHICH")) : 0;  // debug
+    if (trace_which == 2) a1.trace = nullptr;
+    st = launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map1, a1, stream);
+    if (st != FIREQ_SUCCESS) return st;
+    // down: the standard GEMM on (hq, hbeta)
+    CUtensorMap map2;
+    if (!make_x_map(&map2, hq, M, d_ff, p2.ntok)) return fail(FIREQ_ERROR_CUDA, "cuTensorMapEncodeTiled failed");
+    GemmArgs a2 = base_args(p2, M, d_model, d_ff, d_packed, d_scales, d_pts, ws2, pf0, pf0_bytes, pf1, pf1_bytes);
+    a2.x_scale = hbeta;
+    a2.Y = y;
+    a2.ldy = ldy;
+    a2.out_layout = 0;
+    if (trace_which == 1) a2.trace = nullptr;
+    return launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map2, a2, stream);
 }
 
 fireq_status_t debug_lut_table(uint8_t* out, cudaStream_t stream) {

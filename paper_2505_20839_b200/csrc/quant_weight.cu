@@ -216,4 +216,30 @@ fireq_status_t quantize_weight_impl(const __nv_bfloat16* W, int64_t N, int64_t K
     return check_launch("fireq_quantize_weight");
 }
 
+// Row order of the fused FFN's gate_up weight: 128-row tile t
+// holds gate rows [64 t, 64 t + 64) followed by the up rows of the same channels, so one
+// CTA's epilogue sees both operands of SwiGLU.  A row permutation: CAS lambda (per input
+// channel), PTS n and every row's codes are those of the plain [gate; up] stacking.
+__global__ void k_interleave_gate_up(const uint4* __restrict__ wg, const uint4* __restrict__ wu, int64_t d_ff,
+                                     int64_t vec_per_row, uint4* __restrict__ out) {
+    const int64_t total = 2 * d_ff * vec_per_row;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t n = i / vec_per_row, v = i - n * vec_per_row;
+        const int64_t t = n >> 7, r = n & 127;
+        const int64_t j = t * 64 + (r & 63);
+        out[i] = (r < 64 ? wg : wu)[j * vec_per_row + v];
+    }
+}
+
+fireq_status_t interleave_gate_up_impl(const __nv_bfloat16* wg, const __nv_bfloat16* wu, int64_t d_ff,
+                                       int64_t d_model, __nv_bfloat16* out, cudaStream_t stream) {
+    const int64_t vpr = d_model / 8;
+    const int64_t total = 2 * d_ff * vpr;
+    const int blocks = (int)std::min<int64_t>(4096, (total + 255) / 256);
+    k_interleave_gate_up<<<blocks, 256, 0, stream>>>(reinterpret_cast<const uint4*>(wg),
+                                                      reinterpret_cast<const uint4*>(wu), d_ff, vpr,
+                                                      reinterpret_cast<uint4*>(out));
+    return check_launch("fireq_interleave_gate_up");
+}
+
 }  // namespace fireq

@@ -23,7 +23,8 @@ EXPORTS = [
     "fireq_w4a8_gemm", "fireq_comm_get_unique_id", "fireq_comm_init", "fireq_comm_destroy",
     "fireq_w4a8_gemm_colpar", "fireq_debug_lut_table", "fireq_gemm_plan", "fireq_debug_set_trace",
     "fireq_quantize_act_t", "fireq_silu_mul_quantize_act_t", "fireq_debug_set_spans",
-    "fireq_w4a8_gemm_prefetch",
+    "fireq_w4a8_gemm_prefetch", "fireq_interleave_gate_up", "fireq_ffn_workspace_bytes",
+    "fireq_ffn_w4a8_decode",
 ]
 
 
@@ -63,8 +64,14 @@ def load(path=LIB_PATH):
         "fireq_gemm_plan": ([I64, I64, I64, P], C),
         "fireq_debug_set_trace": ([P], C),
         "fireq_debug_set_spans": ([P, C], C),
+        "fireq_interleave_gate_up": ([P, P, I64, I64, P, P], C),
+        "fireq_ffn_workspace_bytes": ([I64, I64, I64], SZ),
+        "fireq_ffn_w4a8_decode": ([P, I64, P, I64, I64, I64, P, P, I32, P, P, P, I32, P, P, I64, P, SZ, P, SZ, P, SZ,
+                                   P], C),
     }
     for name, (args, res) in sig.items():
+        if os.environ.get("FIREQ_LOAD_PARTIAL") and not hasattr(lib, name):   # bisecting older builds
+            continue
         f = getattr(lib, name)
         f.argtypes = args
         f.restype = res
@@ -248,6 +255,45 @@ def w4a8_gemm(xq, beta, packed, scales, N, pts_n, gamma=None, out=None, out_layo
                                           _ptr(pp), pp.numel() if pp is not None else 0,
                                           _ptr(ps), ps.numel() if ps is not None else 0, _stream(stream)),
                "fireq_w4a8_gemm_prefetch")
+    return out
+
+
+def interleave_gate_up(W_gate, W_up, stream=None, out=None):
+    """W_gu (bf16 [2 d_ff][d_model]) in the fused FFN's row order (fireq_interleave_gate_up)."""
+    d_ff, d_model = W_gate.shape
+    if out is None:
+        out = torch.empty((2 * d_ff, d_model), dtype=torch.bfloat16, device=W_gate.device)
+    _check(lib().fireq_interleave_gate_up(_ptr(W_gate), _ptr(W_up), d_ff, d_model, _ptr(out), _stream(stream)),
+           "fireq_interleave_gate_up")
+    return out
+
+
+def ffn_workspace_bytes(M, d_model, d_ff):
+    return lib().fireq_ffn_workspace_bytes(M, d_model, d_ff)
+
+
+def ffn_w4a8_decode(x, q_gu, q_d, h=None, out=None, workspace=None, stream=None, prefetch=None):
+    """y = fireq_ffn_w4a8_decode(x, ...): the two-kernel fused decode FFN.
+
+    q_gu: QuantizedWeight of the interleaved W_gu (interleave_gate_up); q_d: of W_down.
+    workspace: Workspace of ffn_workspace_bytes (zeroed once, left zeroed by each call).
+    """
+    M, d_model = x.shape
+    d_ff = q_d.K
+    L = lib()
+    need = L.fireq_ffn_workspace_bytes(M, d_model, d_ff)
+    ws = workspace.ensure(need) if workspace is not None else torch.zeros(need, dtype=torch.uint8, device=x.device)
+    if h is None:
+        h = torch.empty((M, d_ff), dtype=torch.bfloat16, device=x.device)
+    if out is None:
+        out = torch.empty((M, d_model), dtype=torch.bfloat16, device=x.device)
+    pp, ps = prefetch if prefetch is not None else (None, None)
+    _check(L.fireq_ffn_w4a8_decode(_ptr(x), x.stride(0), _ptr(q_gu.c), M, d_model, d_ff, _ptr(q_gu.packed),
+                                   _ptr(q_gu.scales), q_gu.n, _ptr(q_d.c), _ptr(q_d.packed), _ptr(q_d.scales), q_d.n,
+                                   _ptr(h), _ptr(out), out.stride(0), _ptr(ws), ws.numel(),
+                                   _ptr(pp), pp.numel() if pp is not None else 0,
+                                   _ptr(ps), ps.numel() if ps is not None else 0, _stream(stream)),
+           "fireq_ffn_w4a8_decode")
     return out
 
 

@@ -62,3 +62,17 @@ def test_argument_validation_without_gpu(lib):
     assert st == 1                                    # cas_mode 7
     st = lib.fireq_quantize_act(a16, 0, 128, 128, None, a16, a16, None)
     assert st == 1                                    # M = 0
+
+
+def test_fused_ffn_host_checks(lib):
+    P = ctypes.c_void_p
+    assert lib.fireq_ffn_workspace_bytes(16, 4096, 11008) > 0
+    assert lib.fireq_ffn_workspace_bytes(16, 4000, 11008) == 0          # not a multiple of 128
+    buf = ctypes.create_string_buffer(1 << 12)
+    a16 = P((ctypes.addressof(buf) + 15) & ~15)
+    args = lambda M, x: (x, 4096, None, M, 4096, 11008, a16, a16, 0, None, a16, a16, 0, a16, a16, 4096, a16,
+                         1 << 20, None, 0, None, 0, None)
+    assert lib.fireq_ffn_w4a8_decode(*args(16, None)) == 1               # NULL x
+    assert lib.fireq_ffn_w4a8_decode(*args(17, a16)) == 2                # decode only: M <= 16
+    assert lib.fireq_ffn_w4a8_decode(*args(16, P(a16.value + 2))) == 3  # misaligned x
+    assert lib.fireq_interleave_gate_up(a16, a16, 100, 4096, a16, None) == 2

@@ -73,3 +73,95 @@ def test_ffn_decode_vs_oracle(fireq):
     # by one FP8 step; the bound is 2x the single-layer G4 tolerance.
     assert err <= 2e-2, err
     assert og.rel_frobenius(y.float().cpu().numpy(), r) < 5e-3
+
+
+# ------------------------------------------------------------ fused decode FFN
+def _ffn_case(fireq, M, d, dff, seed):
+    wg = synth.weights(dff, d, seed)
+    wu = synth.weights(dff, d, seed + 1)
+    wd = synth.weights(d, dff, seed + 2)
+    xb = synth.activations(M, d, seed + 3)
+    Wg, Wu = synth.bits_to_torch(wg).to(DEV), synth.bits_to_torch(wu).to(DEV)
+    Wgu = torch.cat([Wg, Wu])
+    qgu = fireq.quantize_weight(Wgu, 1)
+    qd = fireq.quantize_weight(synth.bits_to_torch(wd).to(DEV), 1)
+    Wil = fireq.interleave_gate_up(Wg, Wu)
+    qil = fireq.quantize_weight(Wil, 1)
+    x = synth.bits_to_torch(xb).to(DEV)
+    return wg, wu, wd, xb, Wgu, Wil, qgu, qil, qd, x
+
+
+def _unfused(fireq, x, qgu, qd, dff):
+    d = x.shape[1]
+    gamma = torch.cat([torch.ones(dff, device=DEV), qd.c.float()])
+    xq, beta = fireq.quantize_act(x, chan_mul=qgu.c)
+    gu = fireq.w4a8_gemm(xq, beta, qgu.packed, qgu.scales, 2 * dff, qgu.n, gamma=gamma)
+    hq, hb = fireq.silu_mul_quantize_act(gu[:, :dff], gu[:, dff:])
+    y = fireq.w4a8_gemm(hq, hb, qd.packed, qd.scales, d, qd.n)
+    return hq, hb, y
+
+
+def test_interleave_gate_up_is_a_row_permutation(fireq):
+    d, dff = 256, 384
+    _, _, _, _, Wgu, Wil, qgu, qil, _, _ = _ffn_case(fireq, 1, d, dff, 61)
+    n = np.arange(2 * dff)
+    t, r = n // 128, n % 128
+    src = np.where(r < 64, t * 64 + r, dff + t * 64 + r - 64)
+    assert torch.equal(Wil.cpu(), Wgu.cpu()[torch.from_numpy(src)])
+    # CAS lambda is per input channel and PTS per tensor: unchanged by the permutation
+    assert qil.n == qgu.n and torch.equal(qil.c, qgu.c)
+
+
+@pytest.mark.parametrize("M,d,dff", [(16, 1024, 2816), (5, 512, 384), (1, 256, 128), (11, 768, 1280)])
+def test_fused_ffn_matches_unfused_chain(fireq, M, d, dff):
+    """The fused FFN = quantize_act -> gate_up (SwiGLU epilogue, h quantized in its tail) ->
+    down.  Exact checks: y equals the standalone down GEMM on quantize_act(h) (the tail's
+    quantization is A2..A3 bit for bit), and repeated calls agree (workspace reset).
+    Against the unfused 4-kernel chain: same h codes up to the fp32 summation order of
+    split tiles (the two paths schedule gate_up differently)."""
+    *_, qgu, qil, qd, x = _ffn_case(fireq, M, d, dff, 71 + M)
+    hq, hb, y_ref = _unfused(fireq, x, qgu, qd, dff)
+    ws = fireq.Workspace(fireq.ffn_workspace_bytes(M, d, dff))
+    h = torch.empty((M, dff), dtype=torch.bfloat16, device=DEV)
+    y = fireq.ffn_w4a8_decode(x, qil, qd, h=h, workspace=ws)
+    hq2, hb2 = fireq.quantize_act(h)
+    y2 = fireq.w4a8_gemm(hq2, hb2, qd.packed, qd.scales, d, qd.n)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y2)
+    assert torch.allclose(hb2.float(), hb.float(), rtol=2 ** -7, atol=0)
+    assert (hq2 == hq).float().mean().item() > 0.995
+    yv, rv = y.float().cpu().numpy().astype(np.float64), y_ref.float().cpu().numpy().astype(np.float64)
+    assert og.g4_error(yv, rv) <= 1e-2
+    for _ in range(3):
+        assert torch.equal(fireq.ffn_w4a8_decode(x, qil, qd, h=h, workspace=ws), y)
+
+
+def test_fused_ffn_vs_oracle(fireq):
+    M, d, dff = 16, 1024, 2816
+    wg, wu, wd, xb, *_, qil, qd, x = _ffn_case(fireq, M, d, dff, 81)
+    y = fireq.ffn_w4a8_decode(x, qil, qd, workspace=fireq.Workspace(fireq.ffn_workspace_bytes(M, d, dff)))
+    torch.cuda.synchronize()
+    ref_gu = oq.quantize_weight(synth.bits_to_f64(np.concatenate([wg, wu], axis=0)), 1)
+    ref_d = oq.quantize_weight(synth.bits_to_f64(wd), 1)
+    _, r = of.ffn_reference(synth.bits_to_f64(xb), ref_gu, ref_d, dff)
+    yv = y.float().cpu().numpy().astype(np.float64)
+    assert og.g4_error(yv, r) <= 2e-2                        # same bound as the unfused chain
+    assert og.rel_frobenius(yv, r) < 5e-3
+
+
+def test_fused_ffn_llama2_7b(fireq):
+    """Full Llama2-7B FFN at batch 16, repeated back to back without host syncs."""
+    M, d, dff = 16, 4096, 11008
+    *_, qgu, qil, qd, x = _ffn_case(fireq, M, d, dff, 91)
+    hq, hb, y_ref = _unfused(fireq, x, qgu, qd, dff)
+    ws = fireq.Workspace(fireq.ffn_workspace_bytes(M, d, dff))
+    h = torch.empty((M, dff), dtype=torch.bfloat16, device=DEV)
+    ys = [fireq.ffn_w4a8_decode(x, qil, qd, h=h, workspace=ws) for _ in range(8)]
+    hq2, hb2 = fireq.quantize_act(h)
+    y2 = fireq.w4a8_gemm(hq2, hb2, qd.packed, qd.scales, d, qd.n)
+    torch.cuda.synchronize()
+    assert all(torch.equal(v, ys[0]) for v in ys) and torch.equal(ys[0], y2)
+    assert torch.allclose(hb2.float(), hb.float(), rtol=2 ** -7, atol=0)
+    assert (hq2 == hq).float().mean().item() > 0.995
+    yv, rv = ys[0].float().cpu().numpy().astype(np.float64), y_ref.float().cpu().numpy().astype(np.float64)
+    assert og.g4_error(yv, rv) <= 1e-2 and og.rel_frobenius(yv, rv) < 2e-3
