@@ -159,7 +159,7 @@ class FFN:
         self.ws1 = F.Workspace(F.gemm_workspace_bytes(M, 2 * D_FF, D_MODEL), dev)
         self.ws2 = F.Workspace(F.gemm_workspace_bytes(M, D_MODEL, D_FF), dev)
 
-    def step(self, r, stream=None, prefetch=True):
+    def step(self, r, stream=None, prefetch=os.environ.get("BENCH_PREFETCH", "1") == "1"):
         """One FFN: each GEMM also streams the next GEMM's weights into L2 once its own loads
         are issued (gate_up -> this step's down; down -> the next step's gate_up)."""
         F = self.F

@@ -319,7 +319,7 @@ __device__ __forceinline__ float div_for_e4m3(float x, float beta, float rcp) {
 // allocator, activation TMA producer (the only role that waits on the previous kernel,
 // PDL), weight TMA producer, MMA issuer.
 template <int NTOK, bool SIGN_SPLIT, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS, int NMMA>
-__global__ void __maxnreg__((NCONV >= 4 ? 80 : NTOK <= 32 ? 88 : NTOK <= 64 ? 96 : 128))
+__global__ void __maxnreg__((NTOK <= 32 ? 88 : NTOK <= 64 ? 96 : 128))
 k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
     using C = Cfg<NTOK, SIGN_SPLIT, NCONV, STAGES, ASTAGES, ACCBUF, GPS, NMMA>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -721,6 +721,13 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
             int slot = 0;
             if (!whole) slot = 2 * blockIdx.x + ((u_first < (long long)tile * a.G) ? 1 : 0);   // first/last segment
             float* part = a.partial + (size_t)slot * NTOK * kTileN;
+            // stream-K tile: contributors c_lo..c_hi in CTA order; c_lo (for which this tile is
+            // its LAST split segment, so the others published long ago) reduces it
+            const long long t0 = (long long)tile * a.G, t1 = t0 + a.G - 1;
+            const int c_lo = whole ? 0 : owner_of(t0, a.U, a.C), c_hi = whole ? 0 : owner_of(t1, a.U, a.C);
+            const bool owner = !whole && (int)blockIdx.x == c_lo;
+            const bool keep_own = owner && C::kFixSlots > 0;      // own partial stays in registers
+            float own[C::kFixSlots > 0 ? NTOK : 1];
             uint32_t peer_dst = 0, peer_bar = 0;
             if (C::kFixSlots > 0 && csplit) {
                 if (cq == 0) {
@@ -738,7 +745,8 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                 if (r == 0) FIREQ_TRACE2(12);
             }
             ptx::named_bar_sync(1, 128);            // sScale visible
-#pragma unroll 1
+            constexpr int kChUnroll = NTOK <= 32 ? NTOK / 16 : 1;   // static indices into own[]
+#pragma unroll kChUnroll
             for (int ch = 0; ch < NTOK / 16; ++ch) {
                 uint32_t v[16];
                 ptx::tmem_ld_x16(tmem + lane_base + (b * NMMA + w_first) * NTOK + ch * 16, v);
@@ -776,6 +784,10 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                         }
                     }
                     emit(accv, ch);
+                } else if (keep_own) {
+#pragma unroll
+                    for (int c = 0; c < 16; ++c)
+                        if (C::kFixSlots > 0) own[(ch * 16 + c) % (C::kFixSlots > 0 ? NTOK : 1)] = __uint_as_float(v[c]);
                 } else {
 #pragma unroll
                     for (int c = 0; c < 16; ++c) part[(ch * 16 + c) * kTileN + r] = __uint_as_float(v[c]);
@@ -786,17 +798,26 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
             if (lane == 0) ptx::mbar_arrive(&accempty[b]);
             if (r == 0) FIREQ_TRACE(6);
             if (!whole) {
-                // deterministic cross-CTA reduction: last arriver sums contributors in CTA order
-                ptx::named_bar_sync(1, 128);         // all partial stores of this CTA issued
-                const long long t0 = (long long)tile * a.G, t1 = t0 + a.G - 1;
-                const int c_lo = owner_of(t0, a.U, a.C), c_hi = owner_of(t1, a.U, a.C);
+                // deterministic cross-CTA reduction: the owner c_lo sums the contributors in CTA
+                // order once the others (c_lo+1 .. c_hi) have published.  Waits only point to
+                // higher CTAs, whose split segment for this tile is their first, and every CTA of
+                // a stream-K grid is resident (C <= SMs), so the spin cannot deadlock.
+                if (!owner || !keep_own) __threadfence();    // partial stores performed (gpu scope)
+                ptx::named_bar_sync(1, 128);         // all partial stores of this CTA performed
                 if (r == 0) {
                     if (sg == 0) FIREQ_TRACE2(10);
-                    // gpu-scope acq_rel: publishes this CTA's partials (bar.sync cumulativity)
-                    // and, for the last arriver, acquires everyone else's.
-                    unsigned prev;
-                    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&a.counters[tile]) : "memory");
-                    misc[1] = (prev == (unsigned)(c_hi - c_lo)) ? 1u : 0u;
+                    if (!owner) {
+                        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&a.counters[tile]) : "memory");
+                    } else {
+                        unsigned seen = 0;
+                        const unsigned want = (unsigned)(c_hi - c_lo);
+                        while (true) {
+                            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(&a.counters[tile]) : "memory");
+                            if (seen >= want) break;
+                            __nanosleep(32);
+                        }
+                    }
+                    misc[1] = owner ? 1u : 0u;
                     if (sg < 4) FIREQ_TRACE2(3 * sg + 1);
                 }
                 ptx::named_bar_sync(1, 128);
@@ -812,8 +833,8 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                     const int slots = last_seg ? (STAGES * C::kWStage) / C::kPartBytes : C::kFixSlots;
                     float accv[C::kFixSlots > 0 ? NTOK : 1];
 #pragma unroll
-                    for (int c = 0; c < NTOK; ++c) accv[c] = 0.0f;
-                    for (int cc0 = c_lo; cc0 <= c_hi; cc0 += slots) {
+                    for (int c = 0; c < NTOK; ++c) accv[c] = own[c % (C::kFixSlots > 0 ? NTOK : 1)];
+                    for (int cc0 = c_lo + 1; cc0 <= c_hi; cc0 += slots) {
                         const int nb = min(slots, c_hi - cc0 + 1);
                         if (r < 32 && ptx::elect_one()) {
                             ptx::mbar_arrive_expect_tx(fixbar, nb * C::kPartBytes);
