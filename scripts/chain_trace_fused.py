@@ -18,7 +18,7 @@ which = int(os.environ.get("FIREQ_TRACE_WHICH", "1"))
 D_FF, D_MODEL = bench.D_FF, bench.D_MODEL
 plan = F.gemm_plan(M, 2 * D_FF, D_MODEL) if which == 1 else F.gemm_plan(M, D_MODEL, D_FF)
 tr = torch.zeros(plan["ctas"] * 32 + 512, dtype=torch.int64, device=dev)
-spans = torch.zeros((6, 2), dtype=torch.int64, device=dev)
+spans = torch.zeros((9, 2), dtype=torch.int64, device=dev)
 F.debug_set_spans(spans)
 g = torch.cuda.CUDAGraph()
 with torch.cuda.graph(g, stream=stream):
@@ -35,15 +35,15 @@ for trial in range(3):
     g.replay()
     torch.cuda.synchronize()
 sp = spans.cpu().numpy().astype(np.uint64).astype(np.float64)
-t0 = sp[2, 0]
-names = ["gate_up+act+swiglu", "down+hquant"]
-for i in range(6):
-    print(f"   {names[i % 2]:20s} start {(sp[i,0]-t0)/1e3:8.2f}  end {(sp[i,1]-t0)/1e3:8.2f} us")
+t0 = sp[3, 0]
+names = ["act_quant(x)", "gate_up+swiglu+hq", "down"]
+for i in range(9):
+    print(f"   {names[i % 3]:20s} start {(sp[i,0]-t0)/1e3:8.2f}  end {(sp[i,1]-t0)/1e3:8.2f} us")
 C = plan["ctas"]
 a = tr.cpu().numpy()
 t16 = a[: C * 16].reshape(-1, 16)[:, :8].astype(np.float64)
 rel = np.where(t16 > 0, (t16 - t0) / 1e3, np.nan)
-print(f"{names[which - 1]}: {plan}")
+print(f"{names[which]}: {plan}")
 for j, nm in enumerate(["start", "setup", "first_data", "mma_done", "epi_done", "end", "drained", "fixup_done"]):
     col = rel[:, j]
     col = col[~np.isnan(col)]
@@ -51,7 +51,7 @@ for j, nm in enumerate(["start", "setup", "first_data", "mma_done", "epi_done", 
         print(f"   {nm:10s} min={col.min():7.2f} med={np.median(col):7.2f} max={col.max():7.2f}  (n={col.size})")
 t2 = a[C * 16 + 512: C * 32 + 512].reshape(-1, 16).astype(np.float64)
 rel2 = np.where(t2 > 0, (t2 - t0) / 1e3, np.nan)
-for slot, nm in ((9, "pdl_done"), (11, "amax_red"), (13, "beta_rdy"), (14, "xres_rdy")):
+for slot, nm in ((15, "grid_bar"),):
     col = rel2[:, slot]
     col = col[~np.isnan(col)]
     if col.size:

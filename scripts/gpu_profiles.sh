@@ -1,7 +1,6 @@
 cd $GRAFT_REPO_ROOT
 make -C paper_2505_20839_b200/csrc -j8 all > /dev/null
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 3 --no-prefill --no-cpu > /dev/null 2> gpurun_out/ncu_launch.err; echo "launches rc=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 3 --no-prefill --no-cpu > /dev/null 2> gpurun_out/ncu_launch.err; echo "launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_w4a8_gemm -s 2 -c 1 -o gpurun_out/prof_gu_m16 python scripts/prof_gemm.py 16 22016 4096 4 > gpurun_out/ncu1.log 2>&1; echo "full1 rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_w4a8_gemm -s 2 -c 1 -o gpurun_out/prof_down_m16 python scripts/prof_gemm.py 16 4096 11008 4 > gpurun_out/ncu2.log 2>&1; echo "full2 rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_w4a8_gemm -s 1 -c 1 -o gpurun_out/prof_gu_m16k python scripts/prof_gemm.py 16384 22016 4096 2 > gpurun_out/ncu3.log 2>&1; echo "full3 rc=$?"
-timeout 900 ncu --set full --clock-control none -k regex:k_act_quant -s 2 -c 2 -o gpurun_out/prof_actq python scripts/prof_gemm.py 16 11008 4096 2 > gpurun_out/ncu4.log 2>&1; echo "full4 rc=$?"
