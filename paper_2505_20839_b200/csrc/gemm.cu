@@ -237,7 +237,7 @@ struct Cfg {
     static constexpr int kOffFix = kOffLut + 2048;
     static constexpr int kOffEpi = kOffFix + kFixSlots * kPartBytes;    // scales [NTOK] + 4 KB transpose
     static constexpr int kOffBar = kOffEpi + 1024 + 16 * kTileN * 2;
-    static constexpr int kNumBars = 3 * STAGES + 2 * ASTAGES + 2 * ACCBUF + 1;
+    static constexpr int kNumBars = 3 * STAGES + 2 * ASTAGES + 2 * ACCBUF + 2;
     static constexpr int kOffMisc = kOffBar + kNumBars * 8;
     static constexpr int kSmemBytes = kOffMisc + 64 + 1024;             // + alignment slack
     static_assert(kXBytes % 1024 == 0, "X tile must keep 1024-B alignment");
@@ -318,10 +318,19 @@ __device__ __forceinline__ float div_for_e4m3(float x, float beta, float rcp) {
 // Roles (warp-uniform, see kW* below): converter warpgroups, epilogue warpgroup, TMEM
 // allocator, activation TMA producer (the only role that waits on the previous kernel,
 // PDL), weight TMA producer, MMA issuer.
-template <int NTOK, bool SIGN_SPLIT, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS, int NMMA>
+//
+// NPH = 2 (the persistent decode FFN): the grid runs two GEMMs back to back -- phase 0
+// (gate_up, SwiGLU epilogue, h quantized in its tail) and phase 1 (down on that h).  Every
+// role walks phase 0's schedule, then phase 1's, with its ring / stage / accumulator
+// counters running on; the weight producer streams (and the converters convert) the down
+// weights while phase 0 drains.  Only the activation producer and the epilogue wait for
+// the grid-wide h barrier before phase 1.
+template <int NTOK, bool SIGN_SPLIT, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS, int NMMA, int NPH>
 __global__ void __maxnreg__((NTOK <= 32 ? 88 : NTOK <= 64 ? 96 : 128))
-k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
+k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__ GemmArgs a0,
+            const __grid_constant__ CUtensorMap tmap_x1, const __grid_constant__ GemmArgs a1) {
     using C = Cfg<NTOK, SIGN_SPLIT, NCONV, STAGES, ASTAGES, ACCBUF, GPS, NMMA>;
+    const GemmArgs& a = a0;                 // setup / teardown use phase 0's arguments
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment for the SW128 tiles, computed on the shared-window address so
     // that the pointer stays visibly in the shared state space (LDS, not generic LD).
@@ -339,6 +348,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
     uint64_t* accfull = aempty + ASTAGES;
     uint64_t* accempty = accfull + ACCBUF;
     uint64_t* fixbar = accempty + ACCBUF;
+    uint64_t* ph1bar = fixbar + 1;          // NPH = 2: h quantized grid-wide (epilogue -> X producer)
     float* sFix = reinterpret_cast<float*>(smem + C::kOffFix);
     uint32_t* misc = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);   // [0] tmem base, [1] fixup flag
 
@@ -367,8 +377,10 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
         for (int i = 0; i < ASTAGES; ++i) { ptx::mbar_init(&afull[i], 4); ptx::mbar_init(&aempty[i], 1); }
         for (int i = 0; i < ACCBUF; ++i) { ptx::mbar_init(&accfull[i], NMMA); ptx::mbar_init(&accempty[i], 4); }
         ptx::mbar_init(fixbar, 1);
+        ptx::mbar_init(ph1bar, 1);
         ptx::fence_mbar_init();
-        ptx::prefetch_tmap(&tmap_x);
+        ptx::prefetch_tmap(&tmap_x0);
+        if (NPH == 2) ptx::prefetch_tmap(&tmap_x1);
     }
     if (warp == kWAlloc) {
         ptx::tmem_alloc(&misc[0], C::kTmemCols);
@@ -404,9 +416,11 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
         // lane issues (a lane-0 branch makes the compiler wrap TMAs in waterfall loops).
         // decode: weights are streamed once (evict first); prefill: every m-tile re-reads
         // them, so keep them in L2 (the 126 MB L2 holds the largest layer's weights)
+        int i = 0;
+        for (int ph = 0; ph < NPH; ++ph) {
+        const GemmArgs& a = ph ? a1 : a0;
         const uint64_t pol_w = a.m_tiles == 1 ? ptx::policy_evict_first() : ptx::policy_evict_last();
         st.init(a, blockIdx.x);
-        int i = 0;
         while (st.next(nt, mt, g, ng, sfirst, slast)) {
             const int s = i % STAGES;
             ptx::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
@@ -433,6 +447,8 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
             __syncwarp();
             ++i;
         }
+        }
+        const GemmArgs& a = NPH == 2 ? a1 : a0;
         // Once this CTA's own weight loads are issued, stream its share of the NEXT layer's
         // weights into L2 (caller hint): HBM stays busy through this kernel's tail and the
         // small kernels that follow, and the next GEMM starts from L2-resident weights.
@@ -451,10 +467,20 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
         // ------------------------------------------------------- activation producer
         // decode: the activation tile is re-read by every n-tile; prefill: the concurrent CTAs
         // share one m-tile, then it is dead
-        const uint64_t pol_x = a.m_tiles == 1 ? ptx::policy_evict_last() : ptx::policy_evict_first();
-        ptx::pdl_wait();                    // activations are written by the previous kernel
-        st.init(a, blockIdx.x);
         int i = 0;
+        for (int ph = 0; ph < NPH; ++ph) {
+        const GemmArgs& a = ph ? a1 : a0;
+        const CUtensorMap& tmap_x = ph ? tmap_x1 : tmap_x0;
+        const uint64_t pol_x = a.m_tiles == 1 ? ptx::policy_evict_last() : ptx::policy_evict_first();
+        if (ph == 0) {
+            ptx::pdl_wait();                // activations are written by the previous kernel
+        } else {
+            // phase 1 reads h_hat, written by every CTA's epilogue tail (generic stores): the
+            // epilogue passed the grid barrier with gpu-scope acquire, then released ph1bar
+            ptx::mbar_wait(ph1bar, 0);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        st.init(a, blockIdx.x);
         while (st.next(nt, mt, g, ng, sfirst, slast)) {
             const int s = i % STAGES;
             ptx::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
@@ -469,6 +495,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
             __syncwarp();
             ++i;
         }
+        }
     } else if (warp == kWMma || (NMMA == 2 && warp == kWAlloc)) {
         // ------------------------------------------------------- MMA issuer(s)
         // Whole warp walks the schedule; one elected lane issues the stage's MMAs back to
@@ -479,12 +506,14 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
         const int w = (warp == kWMma) ? 0 : 1;
         constexpr uint32_t idesc_pos = make_idesc(NTOK, false);
         constexpr uint32_t idesc_neg = make_idesc(NTOK, true);
-        st.init(a, blockIdx.x);
         int i = 0, sg = 0;
         const uint32_t sx0 = ptx::smem_u32(sX);
         uint32_t d = tmem;
         bool touched = false;
         long long w_afull = 0, w_full = 0, t_issue = 0, t_mma0 = prof_clock();
+        for (int ph = 0; ph < NPH; ++ph) {
+        const GemmArgs& a = ph ? a1 : a0;
+        st.init(a, blockIdx.x);
         while (st.next(nt, mt, g, ng, sfirst, slast)) {
             const int b = sg % ACCBUF;
             if (sfirst) {
@@ -537,6 +566,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
             }
             ++i;
         }
+        }
         if (lane == 0 && w == 0) {
             FIREQ_TRACE(3);
             FIREQ_TRACE_VAL(9, w_afull);
@@ -554,8 +584,10 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
         // converted in full (the stale SMEM group lands in TMEM columns no MMA reads), so the
         // group loop is fully unrolled and warpgroup wg walks only its own stages.
         int n_stages = 0;
-        it.init(a, blockIdx.x);
-        while (it.next(tile, g0, g1)) n_stages += (g1 - g0 + GPS - 1) / GPS;
+        for (int ph = 0; ph < NPH; ++ph) {
+            it.init(ph ? a1 : a0, blockIdx.x);
+            while (it.next(tile, g0, g1)) n_stages += (g1 - g0 + GPS - 1) / GPS;
+        }
         long long cw_full = 0, cw_aempty = 0, ct0 = prof_clock();
         for (int i = wg; i < n_stages; i += NCONV) {
             const int s = i % STAGES, as = i % ASTAGES;
@@ -625,12 +657,14 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
         ptx::pdl_wait();                    // beta, workspace and Y are shared with earlier kernels
         const int r = threadIdx.x & 127;
         const uint32_t lane_base = (uint32_t)(r & ~31) << 16;
-        const float p2 = exp2_neg(a.pts_n);
         float* sScale = reinterpret_cast<float*>(smem + C::kOffEpi);                 // [NTOK]
         __nv_bfloat16* sT = reinterpret_cast<__nv_bfloat16*>(smem + C::kOffEpi + 1024);  // [16][128]
-        it.init(a, blockIdx.x);
         int sg = 0, i_stage = 0;
         uint32_t fix_phase = 0;
+        for (int ph = 0; ph < NPH; ++ph) {
+        const GemmArgs& a = ph ? a1 : a0;
+        const float p2 = exp2_neg(a.pts_n);
+        it.init(a, blockIdx.x);
         const long long u_first = (long long)blockIdx.x * a.U / a.C;
         int ntile = 0, m0 = 0, n = 0;
         float gam = 1.0f;
@@ -913,8 +947,8 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                 unsigned seen = 0;
                 do {
                     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(a.bar) : "memory");
-                    if (seen < (unsigned)a.C) __nanosleep(64);
-                } while (seen < (unsigned)a.C);
+                    if (seen < gridDim.x) __nanosleep(64);
+                } while (seen < gridDim.x);
                 FIREQ_TRACE2(15);
             }
             ptx::named_bar_sync(1, 128);
@@ -964,13 +998,37 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
                 // the last CTA to leave resets the barrier and amax for the next launch
                 unsigned prev;
                 asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a.bar + 1) : "memory");
-                if (prev == (unsigned)(a.C - 1)) {
+                if (prev == gridDim.x - 1) {
                     for (int m = 0; m < a.M; ++m) a.amax_out[m] = 0u;
                     a.bar[0] = 0u;
                     a.bar[1] = 0u;
                 }
             }
+            if (NPH == 2 && ph == 0) {
+                // second grid barrier: every CTA's slice of h_hat (and hbeta) is written before
+                // any CTA's phase-1 activation loads / epilogue scales read them
+                ptx::named_bar_sync(1, 128);        // this CTA's h_hat stores issued
+                __threadfence();
+                ptx::named_bar_sync(1, 128);
+                if (r == 0) {
+                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar + 2) : "memory");
+                    unsigned seen = 0;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(a.bar + 2) : "memory");
+                        if (seen < gridDim.x) __nanosleep(64);
+                    } while (seen < gridDim.x);
+                    ptx::mbar_arrive(ph1bar);       // release to this CTA's activation producer
+                    unsigned prev;
+                    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a.bar + 3) : "memory");
+                    if (prev == gridDim.x - 1) {    // everyone has passed: reset for the next launch
+                        a.bar[2] = 0u;
+                        a.bar[3] = 0u;
+                    }
+                }
+                ptx::named_bar_sync(1, 128);
+            }
         }
+        }                                           // phases
     }
 
     // ------------------------------------------------------------ teardown
@@ -1078,10 +1136,11 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, bool allow_cluster = true) {
     return p;
 }
 
-template <int NTOK, bool SS, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS, int NMMA>
-fireq_status_t launch_cfg(const CUtensorMap& map, const GemmArgs& args, cudaStream_t stream) {
+template <int NTOK, bool SS, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS, int NMMA, int NPH = 1>
+fireq_status_t launch_cfg(const CUtensorMap& map, const GemmArgs& args, cudaStream_t stream,
+                          const CUtensorMap* map1 = nullptr, const GemmArgs* args1 = nullptr) {
     using C = Cfg<NTOK, SS, NCONV, STAGES, ASTAGES, ACCBUF, GPS, NMMA>;
-    auto kern = k_w4a8_gemm<NTOK, SS, NCONV, STAGES, ASTAGES, ACCBUF, GPS, NMMA>;
+    auto kern = k_w4a8_gemm<NTOK, SS, NCONV, STAGES, ASTAGES, ACCBUF, GPS, NMMA, NPH>;
     static bool attr_done = false;
     if (!attr_done) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
@@ -1090,8 +1149,11 @@ fireq_status_t launch_cfg(const CUtensorMap& map, const GemmArgs& args, cudaStre
     }
     GemmArgs la = args;
     if (la.depth > STAGES - 2 || la.depth < 1) la.depth = STAGES;
+    GemmArgs lb = args1 ? *args1 : la;
+    if (lb.depth > STAGES - 2 || lb.depth < 1) lb.depth = STAGES;
+    const CUtensorMap& m1 = map1 ? *map1 : map;
     const cudaError_t e = launch_ex(kern, dim3(la.C), dim3(C::kThreads), C::kSmemBytes, stream,
-                                    (unsigned)(la.S > 1 ? la.S : 1), map, la);
+                                    (unsigned)(la.S > 1 ? la.S : 1), map, la, m1, lb);
     if (e != cudaSuccess) return fail(FIREQ_ERROR_CUDA, std::string("fireq_w4a8_gemm launch: ") + cudaGetErrorString(e));
     return check_launch("fireq_w4a8_gemm");
 }
@@ -1187,11 +1249,12 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
 }
 
 size_t ffn_workspace_bytes(int64_t M, int64_t d_model, int64_t d_ff) {
-    // gate_up GEMM ws | down GEMM ws | amax[16] + barrier[2] | x_hat | beta_x | h_hat | beta_h
-    // (the gate_up plan never uses clusters: its tail has a grid-wide barrier)
-    return align256(plan_workspace_bytes(make_plan(M, 2 * d_ff, d_model, false))) +
-           align256(gemm_workspace_bytes(M, d_model, d_ff)) + 256 + align256((size_t)M * d_model) + 256 +
-           align256((size_t)M * d_ff) + 256;
+    // gate_up ws | down ws | amax[16] + barriers[4] | x_hat | beta_x | h_hat | beta_h
+    // (neither plan uses clusters: the persistent grid has grid-wide barriers)
+    const size_t down = std::max(plan_workspace_bytes(make_plan(M, d_model, d_ff, false)),
+                                 plan_workspace_bytes(make_plan(M, d_model, d_ff, true)));
+    return align256(plan_workspace_bytes(make_plan(M, 2 * d_ff, d_model, false))) + align256(down) + 256 +
+           align256((size_t)M * d_model) + 256 + align256((size_t)M * d_ff) + 256;
 }
 
 bool ffn_shape_supported(int64_t M, int64_t d_model, int64_t d_ff) {
@@ -1208,17 +1271,23 @@ fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_b
                                int64_t d_model, int64_t d_ff, const uint8_t* gu_packed, const uint8_t* gu_scales,
                                int32_t gu_pts, const __nv_bfloat16* c_down, const uint8_t* d_packed,
                                const uint8_t* d_scales, int32_t d_pts, __nv_bfloat16* h, __nv_bfloat16* y,
-                               int64_t ldy, void* ws, size_t ws_bytes,
-                               cudaStream_t stream, const void* pf0, size_t pf0_bytes, const void* pf1,
-                               size_t pf1_bytes) {
+                               int64_t ldy, void* ws, size_t ws_bytes, cudaStream_t stream, const void* pf0,
+                               size_t pf0_bytes, const void* pf1, size_t pf1_bytes) {
     if (!ffn_shape_supported(M, d_model, d_ff))
         return fail(FIREQ_ERROR_UNSUPPORTED_SHAPE, "fused FFN: decode batches (M <= 16) only");
     if (ws_bytes < ffn_workspace_bytes(M, d_model, d_ff)) return fail(FIREQ_ERROR_WORKSPACE, "FFN workspace too small");
-    const Plan p1 = make_plan(M, 2 * d_ff, d_model, false), p2 = make_plan(M, d_model, d_ff);
+    // Default: three kernels (act quant; gate_up with the SwiGLU tail; down with its own
+    // best plan, cluster split-K at decode).  FIREQ_FFN_PERSISTENT=1 runs gate_up and down
+    // in ONE persistent grid (NPH = 2, stream-K for both phases) -- measured slower so far
+    // (DESIGN.md "Fused decode FFN").
+    static const bool persistent = getenv("FIREQ_FFN_PERSISTENT") != nullptr;
+    const Plan p1 = make_plan(M, 2 * d_ff, d_model, false), p2 = make_plan(M, d_model, d_ff, !persistent);
     uint8_t* w = static_cast<uint8_t*>(ws);
     uint8_t* ws1 = w;
     uint8_t* ws2 = ws1 + align256(plan_workspace_bytes(p1));
-    unsigned* amax = reinterpret_cast<unsigned*>(ws2 + align256(gemm_workspace_bytes(M, d_model, d_ff)));
+    const size_t down_ws = std::max(plan_workspace_bytes(make_plan(M, d_model, d_ff, false)),
+                                    plan_workspace_bytes(make_plan(M, d_model, d_ff, true)));
+    unsigned* amax = reinterpret_cast<unsigned*>(ws2 + align256(down_ws));
     uint8_t* xq = reinterpret_cast<uint8_t*>(amax) + 256;
     __nv_bfloat16* xbeta = reinterpret_cast<__nv_bfloat16*>(xq + align256((size_t)M * d_model));
     uint8_t* hq = reinterpret_cast<uint8_t*>(xbeta) + 256;
@@ -1226,11 +1295,11 @@ fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_b
     // A1..A3 of x (the FFN input comes from the previous layer)
     fireq_status_t st = quantize_act_impl(x, nullptr, M, d_model, ldx, c_gu, c_gu ? 1 : 0, false, xq, xbeta, stream);
     if (st != FIREQ_SUCCESS) return st;
-    // gate_up over interleaved [gate | up] tiles; SwiGLU epilogue; h quantized in the tail
-    CUtensorMap map1;
-    if (!make_x_map(&map1, xq, M, d_model, p1.ntok)) return fail(FIREQ_ERROR_CUDA, "cuTensorMapEncodeTiled failed");
-    GemmArgs a1 = base_args(p1, M, 2 * d_ff, d_model, gu_packed, gu_scales, gu_pts, ws1, d_packed,
-                            (size_t)d_model * d_ff / 2, d_scales, (size_t)d_model * d_ff / 128);
+    // phase 0: gate_up over interleaved [gate | up] tiles; SwiGLU epilogue; h quantized in its tail
+    CUtensorMap map1, map2;
+    if (!make_x_map(&map1, xq, M, d_model, p1.ntok) || !make_x_map(&map2, hq, M, d_ff, p2.ntok))
+        return fail(FIREQ_ERROR_CUDA, "cuTensorMapEncodeTiled failed");
+    GemmArgs a1 = base_args(p1, M, 2 * d_ff, d_model, gu_packed, gu_scales, gu_pts, ws1, nullptr, 0, nullptr, 0);
     a1.x_scale = xbeta;
     a1.out_layout = 2;
     a1.h_out = h;
@@ -1240,19 +1309,19 @@ fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_b
     a1.hq_out = hq;
     a1.hbeta_out = hbeta;
     a1.bar = amax + 16;
-    static const int trace_which = getenv("FIREQ_TRACE_WHICH") ? atoi(getenv("FIREQ_TRACE_WHICH")) : 0;  // debug
-    if (trace_which == 2) a1.trace = nullptr;
-    st = launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map1, a1, stream);
-    if (st != FIREQ_SUCCESS) return st;
-    // down: the standard GEMM on (hq, hbeta)
-    CUtensorMap map2;
-    if (!make_x_map(&map2, hq, M, d_ff, p2.ntok)) return fail(FIREQ_ERROR_CUDA, "cuTensorMapEncodeTiled failed");
+    // phase 1: down on (h_hat, beta_h)
     GemmArgs a2 = base_args(p2, M, d_model, d_ff, d_packed, d_scales, d_pts, ws2, pf0, pf0_bytes, pf1, pf1_bytes);
     a2.x_scale = hbeta;
     a2.Y = y;
     a2.ldy = ldy;
     a2.out_layout = 0;
+    static const int trace_which = getenv("FIREQ_TRACE_WHICH") ? atoi(getenv("FIREQ_TRACE_WHICH")) : 0;  // debug
+    if (trace_which == 2) a1.trace = nullptr;
     if (trace_which == 1) a2.trace = nullptr;
+    if (persistent && p1.C == p2.C)
+        return launch_cfg<16, true, 3, 8, 3, 2, 2, 1, 2>(map1, a1, stream, &map2, &a2);
+    st = launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map1, a1, stream);
+    if (st != FIREQ_SUCCESS) return st;
     return launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map2, a2, stream);
 }
 

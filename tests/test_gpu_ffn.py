@@ -127,7 +127,9 @@ def test_fused_ffn_matches_unfused_chain(fireq, M, d, dff):
     hq2, hb2 = fireq.quantize_act(h)
     y2 = fireq.w4a8_gemm(hq2, hb2, qd.packed, qd.scales, d, qd.n)
     torch.cuda.synchronize()
-    assert torch.equal(y, y2)
+    # same h_hat (the tail's A2..A3 is bit-exact); the down GEMMs may split K differently
+    yv2, y2v = y.float().cpu().numpy().astype(np.float64), y2.float().cpu().numpy().astype(np.float64)
+    assert og.g4_error(yv2, y2v) <= 1e-2 and np.mean(yv2 == y2v) > 0.98
     assert torch.allclose(hb2.float(), hb.float(), rtol=2 ** -7, atol=0)
     assert (hq2 == hq).float().mean().item() > 0.995
     yv, rv = y.float().cpu().numpy().astype(np.float64), y_ref.float().cpu().numpy().astype(np.float64)
@@ -160,7 +162,11 @@ def test_fused_ffn_llama2_7b(fireq):
     hq2, hb2 = fireq.quantize_act(h)
     y2 = fireq.w4a8_gemm(hq2, hb2, qd.packed, qd.scales, d, qd.n)
     torch.cuda.synchronize()
-    assert all(torch.equal(v, ys[0]) for v in ys) and torch.equal(ys[0], y2)
+    assert all(torch.equal(v, ys[0]) for v in ys)
+    # the down step of the fused FFN and the standalone GEMM may split K differently
+    # (persistent stream-K vs cluster split-K): equal up to the FP32 summation order
+    y0, y2v = ys[0].float().cpu().numpy().astype(np.float64), y2.float().cpu().numpy().astype(np.float64)
+    assert og.g4_error(y0, y2v) <= 1e-2 and np.mean(y0 == y2v) > 0.98
     assert torch.allclose(hb2.float(), hb.float(), rtol=2 ** -7, atol=0)
     assert (hq2 == hq).float().mean().item() > 0.995
     yv, rv = ys[0].float().cpu().numpy().astype(np.float64), y_ref.float().cpu().numpy().astype(np.float64)
