@@ -62,7 +62,7 @@ struct GemmArgs {
     int out_layout;
     int R;                 // tiles [0, R) are split contiguously over CTAs ("stream-K")
     int C;                 // CTAs in the grid
-    long long U;           // stream-K units = R * G
+    unsigned U;            // stream-K units = R * G (< 2^31: R < 2 * SMs, G <= K / 128)
     int S;                 // > 1: cluster split-K, one tile per cluster of S CTAs (K split S ways)
     int depth;             // weight stages in flight (<= STAGES): bounds the loaded HBM latency
     // out_layout 2 (SwiGLU pairs): tile rows [0, 64) are gate channels j0 + r, rows [64, 128)
@@ -104,6 +104,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #if FIREQ_PROFILE
 #define FIREQ_TRACE(slot) do { if (a.trace) a.trace[blockIdx.x * 16 + (slot)] = gtimer(); } while (0)
 #define FIREQ_TRACE_VAL(slot, v) do { if (a.trace) a.trace[blockIdx.x * 16 + (slot)] = (v); } while (0)
+#define FIREQ_TRACE_X(slot) do { if (a.trace && (a.dbg & 64)) a.trace[blockIdx.x * 16 + (slot)] = gtimer(); } while (0)
 // per-stage event log of CTA 0: trace[C*16 + stage*8 + ev] (first 64 stages)
 #define FIREQ_EVT(stage, ev) do { if (a.trace && blockIdx.x == 0 && (stage) < 64) \
     a.trace[a.C * 16 + (stage) * 8 + (ev)] = clock64(); } while (0)
@@ -113,6 +114,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #else
 #define FIREQ_TRACE(slot) do { } while (0)
 #define FIREQ_TRACE_VAL(slot, v) do { } while (0)
+#define FIREQ_TRACE_X(slot) do { } while (0)
 #define FIREQ_EVT(stage, ev) do { } while (0)
 #define FIREQ_TRACE2(slot) do { } while (0)
 #endif
@@ -123,11 +125,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // whole tiles R + c, R + c + C, ...
 struct SegIter {
     int G, tiles, C, c, R, k, S;
-    long long u, u_end;
+    unsigned u, u_end;     // 32-bit schedule math: 64-bit division is a slow called routine
     __device__ __forceinline__ void init(const GemmArgs& a, int cta) {
         G = a.G; tiles = a.tiles; C = a.C; c = cta; R = a.R; k = 0; S = a.S;
-        u = a.U ? (long long)cta * a.U / a.C : 0;
-        u_end = a.U ? (long long)(cta + 1) * a.U / a.C : 0;
+        u = a.U ? (unsigned)cta * a.U / (unsigned)a.C : 0u;
+        u_end = a.U ? (unsigned)(cta + 1) * a.U / (unsigned)a.C : 0u;
     }
     __device__ __forceinline__ bool next(int& tile, int& g0, int& g1) {
         if (S > 1) {
@@ -140,10 +142,10 @@ struct SegIter {
             return true;
         }
         if (u < u_end) {
-            tile = (int)(u / G);
-            g0 = (int)(u % G);
-            g1 = (int)min((long long)G, (long long)g0 + (u_end - u));
-            u = (long long)tile * G + g1;
+            tile = (int)(u / (unsigned)G);
+            g0 = (int)(u - (unsigned)tile * (unsigned)G);
+            g1 = (int)min((unsigned)G, (unsigned)g0 + (u_end - u));
+            u = (unsigned)tile * (unsigned)G + (unsigned)g1;
             return true;
         }
         tile = R + c + k * C;
@@ -183,10 +185,10 @@ struct UnitIter {
 };
 
 // CTA owning unit u under the contiguous split.
-__device__ __forceinline__ int owner_of(long long u, long long U, int C) {
-    int c = (int)((u * C) / U);
-    while (c + 1 < C && (long long)(c + 1) * U / C <= u) ++c;
-    while (c > 0 && (long long)c * U / C > u) --c;
+__device__ __forceinline__ int owner_of(unsigned u, unsigned U, int C) {
+    int c = (int)((u * (unsigned)C) / U);
+    while (c + 1 < C && (unsigned)(c + 1) * U / (unsigned)C <= u) ++c;
+    while (c > 0 && (unsigned)c * U / (unsigned)C > u) --c;
     return c;
 }
 
@@ -225,6 +227,13 @@ struct Cfg {
                                    : kTmemNeed <= 256 ? 256 : 512;
     static_assert(kTmemNeed <= 512, "TMEM budget");
     static constexpr int kThreads = 256 + 128 * NCONV;
+    // Decode: the activation tile of stage i completes on the A-stage barrier afull[i % ASTAGES]
+    // together with the converters' arrivals, so the MMA warp waits on ONE barrier per stage
+    // (each mbarrier poll costs the issuing warp 100-300 cycles while the converters load the
+    // shared-memory pipe).  The X producer then runs at most ASTAGES stages ahead (X is a hot,
+    // L2-resident 4 KB tile at decode).  Prefill keeps the separate fullX ring (X from HBM).
+    static constexpr bool kFoldX = NTOK <= 32;
+    static_assert(!kFoldX || ASTAGES < STAGES, "folded X: the A ring must be shorter than the SMEM ring");
     // stream-K fixup: contributor partials are staged into SMEM by bulk copies,
     // kFixSlots per round trip (decode tile sizes only; larger NTOK use registers).
     static constexpr int kFixSlots = NTOK <= 32 ? 32768 / (NTOK * kTileN * 4) : 0;
@@ -374,17 +383,53 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             ptx::mbar_init(&empty[i], 1);
         }
         // afull / accempty: one arrival per warp of the 4-warp group (after __syncwarp)
-        for (int i = 0; i < ASTAGES; ++i) { ptx::mbar_init(&afull[i], 4); ptx::mbar_init(&aempty[i], 1); }
+        for (int i = 0; i < ASTAGES; ++i) { ptx::mbar_init(&afull[i], C::kFoldX ? 5 : 4); ptx::mbar_init(&aempty[i], 1); }
         for (int i = 0; i < ACCBUF; ++i) { ptx::mbar_init(&accfull[i], NMMA); ptx::mbar_init(&accempty[i], 4); }
         ptx::mbar_init(fixbar, 1);
         ptx::mbar_init(ph1bar, 1);
         ptx::fence_mbar_init();
         ptx::prefetch_tmap(&tmap_x0);
         if (NPH == 2) ptx::prefetch_tmap(&tmap_x1);
+        FIREQ_TRACE_X(9);
+    }
+    // Weight stream first: the producer warp issues the first ring's worth of phase 0's weight
+    // loads right after initializing the barriers -- before the LUT build, the TMEM allocation
+    // and the block barrier -- so the DRAM latency of the first stages overlaps the whole setup
+    // (the ring slots are fresh, no empty waits; the loads only touch the W / sigma ring).
+    StageIter<GPS> st;
+    int nt, mt, g, ng;
+    bool sfirst, slast;
+    int w_issued = 0;
+    // (two stages: the TMA engine accepts a 16 KB stage only every ~500 cycles, so a whole ring
+    // issued here would hold the producer warp -- and the block barrier -- for ~2 us)
+    static_assert(STAGES >= 2, "ring");
+    const int w_early = (a0.dbg & 16) ? 0 : (a0.dbg & 32) ? STAGES : a0.depth < 2 ? 1 : 2;   // dbg 16/32: experiments
+    const uint64_t pol_w0 = a0.m_tiles == 1 ? ptx::policy_evict_first() : ptx::policy_evict_last();
+    auto issue_w = [&](const GemmArgs& a, int i, uint64_t pol_w) {
+        const int s = i % STAGES;
+        if (lane == 0) FIREQ_EVT(i, 0);
+        if (lane == 0 && i == 0) FIREQ_TRACE(8);
+        if (ptx::elect_one()) {
+            if (a.dbg & 4) {
+                ptx::mbar_arrive(&fullW[s]);
+            } else {
+                ptx::mbar_arrive_expect_tx(&fullW[s], ng * (kWBytes + kTileN));
+                const size_t blk = (size_t)nt * a.G + g;
+                ptx::bulk_g2s(sW + s * C::kWStage, a.w_packed + blk * kWBytes, ng * kWBytes, &fullW[s], pol_w);
+                ptx::bulk_g2s(sS + s * C::kSStage, a.w_scales + blk * kTileN, ng * kTileN, &fullW[s], pol_w);
+            }
+        }
+        __syncwarp();
+    };
+    if (warp == kWProdW) {
+        __syncwarp();                          // lane 0's barrier inits precede the issues
+        st.init(a0, blockIdx.x);
+        while (w_issued < w_early && st.next(nt, mt, g, ng, sfirst, slast)) issue_w(a0, w_issued++, pol_w0);
     }
     if (warp == kWAlloc) {
         ptx::tmem_alloc(&misc[0], C::kTmemCols);
         ptx::tmem_relinquish();
+        if (lane == 0) FIREQ_TRACE_X(10);
     }
     {
         // LUT-of-LUTs: entry [s][u] = E4M3_RN(v(u) * sigma_s) for all 127 finite sigma codes
@@ -395,6 +440,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             const float v = (float)(u < 8 ? u : u - 16);
             lut[e] = (uint8_t)e4m3_rn(__fmul_rn(v, e4m3_decode((uint32_t)s)));
         }
+        if (threadIdx.x == 0) FIREQ_TRACE_X(12);
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -402,12 +448,10 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
     if (a.S > 1) ptx::cluster_sync();       // peers' mbarrier inits visible before any st.async
     const uint32_t tmem = misc[0];
     if (threadIdx.x == 0) FIREQ_TRACE(1);
+    if (threadIdx.x == 0) FIREQ_TRACE_X(13);   // after the barrier is really released: misc[0] read
 
     SegIter it;
     int tile, g0, g1;
-    StageIter<GPS> st;
-    int nt, mt, g, ng;
-    bool sfirst, slast;
 
     if (warp == kWProdW) {
         // ------------------------------------------------------- weight producer
@@ -416,11 +460,11 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         // lane issues (a lane-0 branch makes the compiler wrap TMAs in waterfall loops).
         // decode: weights are streamed once (evict first); prefill: every m-tile re-reads
         // them, so keep them in L2 (the 126 MB L2 holds the largest layer's weights)
-        int i = 0;
+        int i = w_issued;
         for (int ph = 0; ph < NPH; ++ph) {
         const GemmArgs& a = ph ? a1 : a0;
-        const uint64_t pol_w = a.m_tiles == 1 ? ptx::policy_evict_first() : ptx::policy_evict_last();
-        st.init(a, blockIdx.x);
+        const uint64_t pol_w = ph == 0 ? pol_w0 : a.m_tiles == 1 ? ptx::policy_evict_first() : ptx::policy_evict_last();
+        if (ph > 0 || w_issued == 0) st.init(a, blockIdx.x);   // phase 0: continue after the early issues
         while (st.next(nt, mt, g, ng, sfirst, slast)) {
             const int s = i % STAGES;
             ptx::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
@@ -433,18 +477,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                 const int j = i - a.depth;
                 ptx::mbar_wait(&empty[j % STAGES], (j / STAGES) & 1);
             }
-            if (lane == 0) FIREQ_EVT(i, 0);
-            if (ptx::elect_one()) {
-                if (a.dbg & 4) {
-                    ptx::mbar_arrive(&fullW[s]);
-                } else {
-                    ptx::mbar_arrive_expect_tx(&fullW[s], ng * (kWBytes + kTileN));
-                    const size_t blk = (size_t)nt * a.G + g;
-                    ptx::bulk_g2s(sW + s * C::kWStage, a.w_packed + blk * kWBytes, ng * kWBytes, &fullW[s], pol_w);
-                    ptx::bulk_g2s(sS + s * C::kSStage, a.w_scales + blk * kTileN, ng * kTileN, &fullW[s], pol_w);
-                }
-            }
-            __syncwarp();
+            issue_w(a, i, pol_w);
             ++i;
         }
         }
@@ -483,14 +516,25 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         st.init(a, blockIdx.x);
         while (st.next(nt, mt, g, ng, sfirst, slast)) {
             const int s = i % STAGES;
-            ptx::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+            // the converters need only the weights, so they run ahead of the previous kernel
+            // (PDL) and fill the TMEM A ring before the activations land
+            uint64_t* xbar = &fullX[s];
+            if (C::kFoldX) {
+                // afull[i % ASTAGES] is free for stage i once the MMAs of stage i - ASTAGES have
+                // completed (their commit; this also frees SMEM slot s, ASTAGES < STAGES)
+                if (i >= ASTAGES) {
+                    const int j = i - ASTAGES;
+                    ptx::mbar_wait(&empty[j % STAGES], (j / STAGES) & 1);
+                }
+                xbar = &afull[i % ASTAGES];
+            } else {
+                ptx::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+            }
             if (ptx::elect_one()) {
-                // own barrier: the converters need only the weights, so they run ahead of the
-                // previous kernel (PDL) and fill the TMEM A ring before the activations land
-                ptx::mbar_arrive_expect_tx(&fullX[s], ng * C::kXBytes);
+                ptx::mbar_arrive_expect_tx(xbar, ng * C::kXBytes);
                 for (int q = 0; q < ng; ++q)
                     ptx::tma_2d_g2s(sX + s * C::kXStage + q * C::kXBytes, &tmap_x, (g + q) * kGroup, mt * NTOK,
-                                    &fullX[s], pol_x);
+                                    xbar, pol_x);
             }
             __syncwarp();
             ++i;
@@ -527,7 +571,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                 ptx::mbar_wait(&afull[as], (i / ASTAGES) & 1);
                 if (lane == 0) FIREQ_EVT(i, 4);
                 const long long c1 = prof_clock();
-                ptx::mbar_wait(&fullX[s], (i / STAGES) & 1);
+                if (!C::kFoldX) ptx::mbar_wait(&fullX[s], (i / STAGES) & 1);
                 if (lane == 0) FIREQ_EVT(i, 5);
                 w_afull += c1 - c0;
                 w_full += prof_clock() - c1;
@@ -567,7 +611,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             ++i;
         }
         }
-        if (lane == 0 && w == 0) {
+        if (lane == 0 && w == 0 && !(a.dbg & 64)) {
             FIREQ_TRACE(3);
             FIREQ_TRACE_VAL(9, w_afull);
             FIREQ_TRACE_VAL(10, w_full);
@@ -647,7 +691,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             if (lane == 0) ptx::mbar_arrive(&afull[as]);
             if (r == 0) FIREQ_EVT(i, 3);
         }
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == 0 && !(a.dbg & 64)) {
             FIREQ_TRACE_VAL(12, cw_full);
             FIREQ_TRACE_VAL(13, cw_aempty);
             FIREQ_TRACE_VAL(14, prof_clock() - ct0);
@@ -665,7 +709,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         const GemmArgs& a = ph ? a1 : a0;
         const float p2 = exp2_neg(a.pts_n);
         it.init(a, blockIdx.x);
-        const long long u_first = (long long)blockIdx.x * a.U / a.C;
+        const unsigned u_first = blockIdx.x * a.U / (unsigned)a.C;
         int ntile = 0, m0 = 0, n = 0;
         float gam = 1.0f;
         const bool use_gam = a.gamma != nullptr || (a.out_layout == 2 && a.gamma_up != nullptr);
@@ -753,11 +797,11 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             const int cq = csplit ? (int)(blockIdx.x % a.S) : 0;
             const int swz = NTOK == 16 ? ((r >> 1) & 3) : (r & 7);
             int slot = 0;
-            if (!whole) slot = 2 * blockIdx.x + ((u_first < (long long)tile * a.G) ? 1 : 0);   // first/last segment
+            if (!whole) slot = 2 * blockIdx.x + ((u_first < (unsigned)tile * (unsigned)a.G) ? 1 : 0);   // first/last segment
             float* part = a.partial + (size_t)slot * NTOK * kTileN;
             // stream-K tile: contributors c_lo..c_hi in CTA order; c_lo (for which this tile is
             // its LAST split segment, so the others published long ago) reduces it
-            const long long t0 = (long long)tile * a.G, t1 = t0 + a.G - 1;
+            const unsigned t0 = (unsigned)tile * (unsigned)a.G, t1 = t0 + (unsigned)a.G - 1u;
             const int c_lo = whole ? 0 : owner_of(t0, a.U, a.C), c_hi = whole ? 0 : owner_of(t1, a.U, a.C);
             const bool owner = !whole && (int)blockIdx.x == c_lo;
             const bool keep_own = owner && C::kFixSlots > 0;      // own partial stays in registers
@@ -874,7 +918,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                             ptx::mbar_arrive_expect_tx(fixbar, nb * C::kPartBytes);
                             for (int q = 0; q < nb; ++q) {
                                 const int cc = cc0 + q;
-                                const long long cu0 = (long long)cc * a.U / a.C;
+                                const unsigned cu0 = (unsigned)cc * a.U / (unsigned)a.C;
                                 const int sl = 2 * cc + ((cu0 < t0) ? 1 : 0);
                                 ptx::bulk_g2s(fixbuf + q * (C::kPartBytes / 4), a.partial + (size_t)sl * NTOK * kTileN,
                                               C::kPartBytes, fixbar, 0ull);
@@ -910,7 +954,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                             for (int q = 0; q < 4; ++q) {
                                 const int cc = cc0 + q;
                                 if (cc <= c_hi) {
-                                    const long long cu0 = (long long)cc * a.U / a.C;
+                                    const unsigned cu0 = (unsigned)cc * a.U / (unsigned)a.C;
                                     const int sl = 2 * cc + ((cu0 < t0) ? 1 : 0);
                                     const float* pp = a.partial + (size_t)sl * NTOK * kTileN;
 #pragma unroll
@@ -1194,7 +1238,7 @@ GemmArgs base_args(const Plan& p, int64_t M, int64_t N, int64_t K, const uint8_t
     args.pts_n = pts_n;
     args.R = p.R;
     args.C = p.C;
-    args.U = p.U;
+    args.U = (unsigned)p.U;
     args.S = p.S;
     {
         static const int depth = getenv("FIREQ_DEPTH") ? atoi(getenv("FIREQ_DEPTH")) : 1000;   // experiments
@@ -1240,7 +1284,14 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
         // <= 96 registers per thread so a CTA of the next small kernel of a PDL chain fits.
         // NMMA = 1: two MMA-issuing warps (separate accumulators) produced rare wrong tiles
         // (~1% of launches, scripts/dbg_det4.py); a single issuer is exact.
-        case 16:  return launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map, args, stream);
+        case 16: {
+            static const int v = getenv("FIREQ_CFG16") ? atoi(getenv("FIREQ_CFG16")) : 0;   // experiments
+            if (v == 1) return launch_cfg<16, false, 3, 8, 6, 2, 2, 1>(map, args, stream);
+            if (v == 2) return launch_cfg<16, false, 3, 4, 3, 2, 4, 1>(map, args, stream);
+            if (v == 3) return launch_cfg<16, false, 3, 6, 3, 2, 3, 1>(map, args, stream);
+            if (v == 4) return launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map, args, stream);
+            return launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map, args, stream);
+        }
         case 32:  return launch_cfg<32, true, 3, 7, 3, 2, 2, 1>(map, args, stream);
         case 64:  return launch_cfg<64, true, 2, 5, 2, 2, 2, 1>(map, args, stream);
         case 128: return launch_cfg<128, true, 2, 7, 4, 2, 1, 1>(map, args, stream);

@@ -139,6 +139,9 @@ class QuantizedWeight:
     def n(self):
         """PTS exponent (reads the device scalar back once, as the C ABI prescribes)."""
         if self._n is None:
+            # the quantizer ran asynchronously on the caller's stream, which need not be the
+            # current one: synchronize the device before the (offline, once) read-back
+            torch.cuda.synchronize(self.pts_and_status.device)
             host = self.pts_and_status.cpu()
             if int(host[1]) != 0:
                 raise FireqError(f"fireq_quantize_weight device status {int(host[1])}")
@@ -163,6 +166,8 @@ def quantize_weight(W, cas_mode=1, stream=None, out=None):
     ws = torch.empty(L.fireq_quantize_weight_workspace_bytes(N, K), dtype=torch.uint8, device=dev)
     _check(L.fireq_quantize_weight(_ptr(W), N, K, cas_mode, _ptr(packed), _ptr(scales), _ptr(lam), _ptr(c),
                                    _ptr(ps), _ptr(ws), ws.numel(), _stream(stream)), "fireq_quantize_weight")
+    if stream is not None:
+        ws.record_stream(stream)          # the scratch is freed while the kernels may still run
     return QuantizedWeight(packed, scales, lam, c, ps, N, K)
 
 

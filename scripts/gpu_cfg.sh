@@ -1,9 +1,3 @@
-# FFN bench + gate_up / down trace per FIREQ_CFG16 variant
+# steady-state slope vs fixed overhead of the decode GEMM: N sweep, L2-resident (ROT=1) vs HBM (ROT=4)
 cd $GRAFT_REPO_ROOT
-make -C paper_2505_20839_b200/csrc -j8 all prof > /dev/null
-for v in ${VARIANTS:-0 1 2 3 4}; do
-  echo "=== FIREQ_CFG16=$v"
-  FIREQ_CFG16=$v timeout 200 python bench.py --no-cpu --no-prefill --steps 1000 > gpurun_out/bench_v$v.json 2> gpurun_out/bench_v$v.err
-  python -c "import json,sys; d=json.load(open('gpurun_out/bench_v$v.json')); print('FFN', d['value'], 'gu', d['roofline']['launch_us'], 'down', d['gemm_down']['us'])"
-  FIREQ_CFG16=$v timeout 300 python scripts/trace_gemm.py 2>&1 | grep -E "^M=16 N=(22016|4096) K=(4096|11008)" -A 8 | grep -E "^M=|first_data|mma_done|end "
-done
+for v in ${CFGS:-0 1}; do for r in 1 4; do echo "== cfg $v ROT=$r"; FIREQ_CFG16=$v ROT=$r timeout 120 python scripts/time_gemm.py 16 5504 4096 16 11008 4096 16 22016 4096 16 44032 4096 16 88064 4096; done; done 2>&1 | tee gpurun_out/cfg.txt

@@ -1,8 +1,7 @@
-# tests + trace + bench
+# quick iteration: GPU parity tests + decode GEMM timings (+ optional trace)
 cd $GRAFT_REPO_ROOT
-make -C paper_2505_20839_b200/csrc -j8 all prof > /dev/null
-timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python -m pytest tests -m gpu -x -q --timeout 300 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 tail -3 gpurun_out/pytest_gpu.log
-timeout 300 python scripts/trace_gemm.py 2>&1 | tail -30
-timeout 600 python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
-cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
+timeout 120 python scripts/time_gemm.py 16 22016 4096 16 4096 11008 16 4096 4096 16 14336 4096 16 4096 14336 2>&1 | tee gpurun_out/time.txt
+[ -n "$TRACE" ] && FIREQ_DEBUG_MODE=64 timeout 100 python scripts/trace_gemm.py 16 22016 4096 2>&1 | head -24
+true

@@ -7,7 +7,11 @@ import synth
 from paper_2505_20839_b200 import fireq as F
 
 F.load(os.path.join(os.path.dirname(F.LIB_PATH), 'libfireq_prof.so'))
-for (M, N, K) in [(16, 22016, 4096), (16, 4096, 11008), (16, 4096, 4096), (16384, 22016, 4096)]:
+SHAPES = [(16, 22016, 4096), (16, 4096, 11008), (16, 4096, 4096), (16384, 22016, 4096)]
+if len(sys.argv) > 3:
+    a = [int(v) for v in sys.argv[1:]]
+    SHAPES = list(zip(a[0::3], a[1::3], a[2::3]))
+for (M, N, K) in SHAPES:
     W = synth.bits_to_torch(synth.weights(N, K, 1)).cuda()
     X = synth.bits_to_torch(synth.activations(M, K, 2)).cuda()
     qw = F.quantize_weight(W, 1)
@@ -16,16 +20,18 @@ for (M, N, K) in [(16, 22016, 4096), (16, 4096, 11008), (16, 4096, 4096), (16384
     out = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
     n = qw.n
     plan = F.gemm_plan(M, N, K)
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    # ROT weight copies launched back to back (HBM-resident, no L2 flush write-back in flight);
+    # the last launch is traced
+    ROT = int(os.environ.get("ROT", "4"))
+    rot = [(qw.packed.clone(), qw.scales.clone()) for _ in range(ROT)]
     tr = torch.zeros(plan["ctas"] * 32 + 512, dtype=torch.int64, device="cuda")
-    for it in range(3):
-        flush.fill_(it)
-        F.debug_set_trace(tr if it == 2 else None)
+    for it in range(2 * ROT + 1):
+        F.debug_set_trace(tr if it == 2 * ROT else None)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        F.w4a8_gemm(xq, beta, qw.packed, qw.scales, N, n, out=out, workspace=ws)
+        F.w4a8_gemm(xq, beta, rot[it % ROT][0], rot[it % ROT][1], N, n, out=out, workspace=ws)
         e1.record()
-        torch.cuda.synchronize()
+    torch.cuda.synchronize()
     F.debug_set_trace(None)
     t16 = tr.cpu().numpy()[: plan["ctas"] * 16].reshape(-1, 16).astype(np.int64)
     t = t16[:, :8]
@@ -38,11 +44,17 @@ for (M, N, K) in [(16, 22016, 4096), (16, 4096, 11008), (16, 4096, 4096), (16384
         col = col[~np.isnan(col)]
         if col.size:
             print(f"   {nm:10s} min={col.min():8.2f} med={np.median(col):8.2f} max={col.max():8.2f} us  (n={col.size})")
+    fw = np.where(t16[:, 8] > 0, (t16[:, 8] - t0) / 1000.0, np.nan)
+    print(f"   first_W_issue min={np.nanmin(fw):8.2f} med={np.nanmedian(fw):8.2f} max={np.nanmax(fw):8.2f} us")
+    if os.environ.get("FIREQ_DEBUG_MODE", "0") == "64":
+        for j, nm in [(9, "bar_init_done"), (10, "tmem_alloc_done"), (12, "lut_done_t0"), (13, "after_syncthreads"), (11, "prod_role_start"), (14, "prod_after_init"), (15, "prod_after_next")]:
+            v = np.where(t16[:, j] > 0, (t16[:, j] - t0) / 1000.0, np.nan)
+            print(f"   {nm:16s} min={np.nanmin(v):8.2f} med={np.nanmedian(v):8.2f} max={np.nanmax(v):8.2f} us")
     cyc = t16[:, 8:16]
-    cn = ["prod_wait_empty", "mma_wait_afull", "mma_wait_full", "mma_total", "conv_wait_full", "conv_wait_aempty", "conv_total", "mma_issue"]
+    cn = ["(first_W_issue)", "mma_wait_afull", "mma_wait_full", "mma_total", "conv_wait_full", "conv_wait_aempty", "conv_total", "mma_issue"]
     for j, nm in enumerate(cn):
         print(f"   cyc {nm:18s} med={np.median(cyc[:, j]):9.0f}")
-    del W, X, qw, flush
+    del W, X, qw, rot
     torch.cuda.empty_cache()
     if os.environ.get("TRACE_SLOW"):
         order = np.argsort(-np.nan_to_num(rel[:, 5]))
