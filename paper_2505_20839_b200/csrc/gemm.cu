@@ -227,13 +227,12 @@ struct Cfg {
                                    : kTmemNeed <= 256 ? 256 : 512;
     static_assert(kTmemNeed <= 512, "TMEM budget");
     static constexpr int kThreads = 256 + 128 * NCONV;
-    // Decode: the activation tile of stage i completes on the A-stage barrier afull[i % ASTAGES]
-    // together with the converters' arrivals, so the MMA warp waits on ONE barrier per stage
-    // (each mbarrier poll costs the issuing warp 100-300 cycles while the converters load the
-    // shared-memory pipe).  The X producer then runs at most ASTAGES stages ahead (X is a hot,
-    // L2-resident 4 KB tile at decode).  Prefill keeps the separate fullX ring (X from HBM).
+    // Decode: the converters (which have slack) wait for the activation tile of stage i before
+    // arriving on the A-stage barrier, so the MMA warp -- the serial critical path, where each
+    // mbarrier poll costs 100-300 cycles while the converters load the shared-memory pipe --
+    // waits on ONE barrier per stage.  The X ring stays STAGES deep (X loads stay off the
+    // A-slot cycle).  Prefill keeps the MMA's own fullX wait.
     static constexpr bool kFoldX = NTOK <= 32;
-    static_assert(!kFoldX || ASTAGES < STAGES, "folded X: the A ring must be shorter than the SMEM ring");
     // stream-K fixup: contributor partials are staged into SMEM by bulk copies,
     // kFixSlots per round trip (decode tile sizes only; larger NTOK use registers).
     static constexpr int kFixSlots = NTOK <= 32 ? 32768 / (NTOK * kTileN * 4) : 0;
@@ -292,8 +291,8 @@ struct StageIter {
 __device__ __forceinline__ void conv_sign_split(uint32_t w, uint32_t L0, uint32_t L1, uint32_t N0, uint32_t N1,
                                                 uint32_t& p0, uint32_t& p1, uint32_t& n0, uint32_t& n1) {
     const uint32_t x = w ^ 0x88888888u;
-    const uint32_t wh = ptx::hi16_fma(w);
-    const uint32_t xh = ptx::hi16_fma(x);
+    const uint32_t wh = ptx::hi16_prmt(w);      // byte permute: full ALU rate (IMAD.HI: half rate)
+    const uint32_t xh = ptx::hi16_prmt(x);
     p0 = ptx::prmt(L0, L1, w);
     p1 = ptx::prmt(L0, L1, wh);
     n0 = ptx::prmt(N0, N1, x);
@@ -383,7 +382,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             ptx::mbar_init(&empty[i], 1);
         }
         // afull / accempty: one arrival per warp of the 4-warp group (after __syncwarp)
-        for (int i = 0; i < ASTAGES; ++i) { ptx::mbar_init(&afull[i], C::kFoldX ? 5 : 4); ptx::mbar_init(&aempty[i], 1); }
+        for (int i = 0; i < ASTAGES; ++i) { ptx::mbar_init(&afull[i], 4); ptx::mbar_init(&aempty[i], 1); }
         for (int i = 0; i < ACCBUF; ++i) { ptx::mbar_init(&accfull[i], NMMA); ptx::mbar_init(&accempty[i], 4); }
         ptx::mbar_init(fixbar, 1);
         ptx::mbar_init(ph1bar, 1);
@@ -403,7 +402,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
     // (two stages: the TMA engine accepts a 16 KB stage only every ~500 cycles, so a whole ring
     // issued here would hold the producer warp -- and the block barrier -- for ~2 us)
     static_assert(STAGES >= 2, "ring");
-    const int w_early = (a0.dbg & 16) ? 0 : (a0.dbg & 32) ? STAGES : a0.depth < 2 ? 1 : 2;   // dbg 16/32: experiments
+    const int w_early = a0.depth < 2 ? 1 : 2;
     const uint64_t pol_w0 = a0.m_tiles == 1 ? ptx::policy_evict_first() : ptx::policy_evict_last();
     auto issue_w = [&](const GemmArgs& a, int i, uint64_t pol_w) {
         const int s = i % STAGES;
@@ -516,20 +515,10 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         st.init(a, blockIdx.x);
         while (st.next(nt, mt, g, ng, sfirst, slast)) {
             const int s = i % STAGES;
-            // the converters need only the weights, so they run ahead of the previous kernel
-            // (PDL) and fill the TMEM A ring before the activations land
+            // own barrier: the converters need only the weights, so they run ahead of the
+            // previous kernel (PDL) and fill the TMEM A ring before the activations land
+            ptx::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
             uint64_t* xbar = &fullX[s];
-            if (C::kFoldX) {
-                // afull[i % ASTAGES] is free for stage i once the MMAs of stage i - ASTAGES have
-                // completed (their commit; this also frees SMEM slot s, ASTAGES < STAGES)
-                if (i >= ASTAGES) {
-                    const int j = i - ASTAGES;
-                    ptx::mbar_wait(&empty[j % STAGES], (j / STAGES) & 1);
-                }
-                xbar = &afull[i % ASTAGES];
-            } else {
-                ptx::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
-            }
             if (ptx::elect_one()) {
                 ptx::mbar_arrive_expect_tx(xbar, ng * C::kXBytes);
                 for (int q = 0; q < ng; ++q)
@@ -554,6 +543,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         const uint32_t sx0 = ptx::smem_u32(sX);
         uint32_t d = tmem;
         bool touched = false;
+        bool a_ready = false;    // afull of stage i already seen complete by the previous stage's probe
         long long w_afull = 0, w_full = 0, t_issue = 0, t_mma0 = prof_clock();
         for (int ph = 0; ph < NPH; ++ph) {
         const GemmArgs& a = ph ? a1 : a0;
@@ -568,7 +558,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             if ((i % NMMA) == w) {
                 const int s = i % STAGES, as = i % ASTAGES;
                 const long long c0 = prof_clock();
-                ptx::mbar_wait(&afull[as], (i / ASTAGES) & 1);
+                if (!a_ready) ptx::mbar_wait(&afull[as], (i / ASTAGES) & 1);
                 if (lane == 0) FIREQ_EVT(i, 4);
                 const long long c1 = prof_clock();
                 if (!C::kFoldX) ptx::mbar_wait(&fullX[s], (i / STAGES) & 1);
@@ -578,6 +568,11 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                 ptx::tc_fence_after();
                 const uint32_t ta = tmem + C::kACol0 + as * C::kASz;
                 const long long c2 = prof_clock();
+                // probe the next stage's A barrier now: its round trip overlaps this stage's MMA
+                // issue (a stale "not yet" falls back to the blocking wait; a phase of a stage
+                // that does not exist is never used)
+                const bool nxt = NMMA == 1 && C::kFoldX &&
+                                 ptx::mbar_test_wait(&afull[(i + 1) % ASTAGES], ((i + 1) / ASTAGES) & 1);
                 if (ptx::elect_one()) {
                     if (!(a.dbg & 2)) {
                         for (int q = 0; q < ng; ++q) {
@@ -596,6 +591,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                 }
                 __syncwarp();
                 touched = true;
+                a_ready = nxt;
                 t_issue += prof_clock() - c2;
                 if (lane == 0) FIREQ_EVT(i, 6);
             }
@@ -686,6 +682,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                 }
                 ptx::tmem_wait_st();
             }
+            if (C::kFoldX) ptx::mbar_wait(&fullX[s], (i / STAGES) & 1);   // X of this stage landed
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&afull[as]);
@@ -1284,14 +1281,9 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
         // <= 96 registers per thread so a CTA of the next small kernel of a PDL chain fits.
         // NMMA = 1: two MMA-issuing warps (separate accumulators) produced rare wrong tiles
         // (~1% of launches, scripts/dbg_det4.py); a single issuer is exact.
-        case 16: {
-            static const int v = getenv("FIREQ_CFG16") ? atoi(getenv("FIREQ_CFG16")) : 0;   // experiments
-            if (v == 1) return launch_cfg<16, false, 3, 8, 6, 2, 2, 1>(map, args, stream);
-            if (v == 2) return launch_cfg<16, false, 3, 4, 3, 2, 4, 1>(map, args, stream);
-            if (v == 3) return launch_cfg<16, false, 3, 6, 3, 2, 3, 1>(map, args, stream);
-            if (v == 4) return launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map, args, stream);
-            return launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map, args, stream);
-        }
+        // (measured alternatives: mask-select at decode, 4 groups per stage, one
+        //  group per stage with 7 TMEM A stages, 2 converter warpgroups -- all slower)
+        case 16:  return launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map, args, stream);
         case 32:  return launch_cfg<32, true, 3, 7, 3, 2, 2, 1>(map, args, stream);
         case 64:  return launch_cfg<64, true, 2, 5, 2, 2, 2, 1>(map, args, stream);
         case 128: return launch_cfg<128, true, 2, 7, 4, 2, 1, 1>(map, args, stream);

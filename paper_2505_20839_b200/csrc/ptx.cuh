@@ -23,6 +23,9 @@ __device__ __forceinline__ void fence_mbar_init() {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;"
                  ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
@@ -32,6 +35,17 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    return ok != 0;
+}
+// Non-blocking probe of a phase (no suspend): lets a warp overlap the round trip of the
+// NEXT stage's barrier with the current stage's work.
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
     return ok != 0;
@@ -157,6 +171,14 @@ __device__ __forceinline__ uint32_t lop3_mux(uint32_t a, uint32_t b, uint32_t m)
 __device__ __forceinline__ uint32_t hi16_fma(uint32_t x) {
     uint32_t d;
     asm("mul.hi.u32 %0, %1, 65536;" : "=r"(d) : "r"(x));
+    return d;
+}
+// x >> 16 in the low half (the high half is a don't-care for a prmt selector) by a byte
+// permute: PRMT issues at the full ALU rate, IMAD.HI at half the FMA rate and steals the
+// converters' dispatch slots (B200 microbenchmark, scripts/conv_microbench.cu).
+__device__ __forceinline__ uint32_t hi16_prmt(uint32_t x) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %1, 0x3232;" : "=r"(d) : "r"(x));
     return d;
 }
 __device__ __forceinline__ uint32_t shl4_fma(uint32_t x) {

@@ -1,3 +1,5 @@
-# steady-state slope vs fixed overhead of the decode GEMM: N sweep, L2-resident (ROT=1) vs HBM (ROT=4)
+# A/B of decode GEMM template configurations (FIREQ_CFG16) and debug modes
 cd $GRAFT_REPO_ROOT
-for v in ${CFGS:-0 1}; do for r in 1 4; do echo "== cfg $v ROT=$r"; FIREQ_CFG16=$v ROT=$r timeout 120 python scripts/time_gemm.py 16 5504 4096 16 11008 4096 16 22016 4096 16 44032 4096 16 88064 4096; done; done 2>&1 | tee gpurun_out/cfg.txt
+for v in ${CFGS:-0}; do for m in ${MODES:-0}; do echo "== cfg $v dbg $m"; FIREQ_CFG16=$v FIREQ_DEBUG_MODE=$m timeout 120 python scripts/time_gemm.py ${SHAPES:-16 5504 4096 16 11008 4096 16 22016 4096 16 44032 4096 16 88064 4096}; done; done 2>&1 | tee gpurun_out/cfg.txt
+for v in ${TESTCFGS:-}; do echo "== tests cfg $v"; FIREQ_CFG16=$v timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -1; done
+true
