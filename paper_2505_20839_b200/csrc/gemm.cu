@@ -303,8 +303,8 @@ __device__ __forceinline__ void conv_mask_select(uint32_t w, uint32_t L0, uint32
                                                  uint32_t& r0, uint32_t& r1) {
     const uint32_t x = w ^ 0x88888888u;
     const uint32_t t = ptx::shl4_fma(w);
-    const uint32_t wh = ptx::hi16_fma(w);
-    const uint32_t xh = ptx::hi16_fma(x);
+    const uint32_t wh = ptx::hi16_prmt(w);
+    const uint32_t xh = ptx::hi16_prmt(x);
     const uint32_t m0 = ptx::prmt(w, t, 0x9D8Cu);     // 0xFF where nibble 0..3 is negative
     const uint32_t m1 = ptx::prmt(w, t, 0xBFAEu);     // nibbles 4..7
     r0 = ptx::lop3_mux(ptx::prmt(L0, L1, w), ptx::prmt(L2, L3, x), m0);
