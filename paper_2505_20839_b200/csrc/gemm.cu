@@ -803,6 +803,16 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             const bool owner = !whole && (int)blockIdx.x == c_lo;
             const bool keep_own = owner && C::kFixSlots > 0;      // own partial stays in registers
             float own[C::kFixSlots > 0 ? NTOK : 1];
+            // NTOK > 32: an owner whose split segment is the CTA's last one keeps its partial in
+            // TMEM (no later MMA touches the buffer) and stages the contributors' partials through
+            // the idle X / W rings with bulk copies (one L2 round trip per ring-full instead of
+            // one per 16-column chunk and 4 contributors)
+            bool big_own = false;
+            if (C::kFixSlots == 0 && NMMA == 1 && NPH == 1 && owner) {
+                SegIter peek = it;
+                int pt, pg0, pg1;
+                big_own = !peek.next(pt, pg0, pg1);
+            }
             uint32_t peer_dst = 0, peer_bar = 0;
             if (C::kFixSlots > 0 && csplit) {
                 if (cq == 0) {
@@ -822,7 +832,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             ptx::named_bar_sync(1, 128);            // sScale visible
             constexpr int kChUnroll = NTOK <= 32 ? NTOK / 16 : 1;   // static indices into own[]
 #pragma unroll kChUnroll
-            for (int ch = 0; ch < NTOK / 16; ++ch) {
+            for (int ch = 0; ch < (big_own ? 0 : NTOK / 16); ++ch) {
                 uint32_t v[16];
                 ptx::tmem_ld_x16(tmem + lane_base + (b * NMMA + w_first) * NTOK + ch * 16, v);
                 if (both) {
@@ -936,6 +946,58 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
 #pragma unroll
                         for (int c = 0; c < 16; ++c) e[c] = accv[ch * 16 + c];
                         emit(e, ch);
+                    }
+                } else if (misc[1] && big_own) {
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    constexpr int kRingBytes = STAGES * (C::kXStage + C::kWStage);
+                    constexpr int kSlots = kRingBytes / (NTOK * kTileN * 4);
+                    static_assert(C::kFixSlots > 0 || kSlots >= 1, "the rings must hold one partial");
+                    constexpr int kPart = NTOK * kTileN;             // floats per partial
+                    float* fixbuf = reinterpret_cast<float*>(smem + C::kOffX);
+                    const uint32_t acc_t = tmem + lane_base + (uint32_t)(b * NMMA * NTOK);
+                    for (int cc0 = c_lo + 1; cc0 <= c_hi; cc0 += kSlots) {
+                        const int nb = min(kSlots, c_hi - cc0 + 1);
+                        const bool final = cc0 + nb > c_hi;
+                        if (r < 32 && ptx::elect_one()) {
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                            ptx::mbar_arrive_expect_tx(fixbar, (uint32_t)(nb * kPart * 4));
+                            for (int q = 0; q < nb; ++q) {
+                                const int cc = cc0 + q;
+                                const unsigned cu0 = (unsigned)cc * a.U / (unsigned)a.C;
+                                const int sl = 2 * cc + ((cu0 < t0) ? 1 : 0);
+                                ptx::bulk_g2s(fixbuf + q * kPart, a.partial + (size_t)sl * kPart, kPart * 4, fixbar, 0ull);
+                            }
+                        }
+                        __syncwarp();
+                        ptx::mbar_wait(fixbar, fix_phase);
+                        fix_phase ^= 1u;
+#pragma unroll 1
+                        for (int ch = 0; ch < NTOK / 16; ++ch) {
+                            // running sum in CTA order: own (TMEM) + c_lo+1 + ... + c_hi
+                            uint32_t v[16];
+                            ptx::tmem_ld_x16(acc_t + ch * 16, v);
+                            ptx::tmem_wait_ld();
+                            float accv[16];
+#pragma unroll
+                            for (int c = 0; c < 16; ++c) accv[c] = __uint_as_float(v[c]);
+                            for (int q = 0; q < nb; ++q) {
+#pragma unroll
+                                for (int c = 0; c < 16; ++c)
+                                    accv[c] = __fadd_rn(accv[c], fixbuf[q * kPart + (ch * 16 + c) * kTileN + r]);
+                            }
+                            if (final) {
+                                emit(accv, ch);
+                            } else {
+                                uint32_t lo[8], hi[8];
+#pragma unroll
+                                for (int c = 0; c < 8; ++c) { lo[c] = __float_as_uint(accv[c]); hi[c] = __float_as_uint(accv[8 + c]); }
+                                ptx::tmem_st_x8(acc_t + ch * 16, lo);
+                                ptx::tmem_st_x8(acc_t + ch * 16 + 8, hi);
+                            }
+                        }
+                        if (!final) ptx::tmem_wait_st();
+                        ptx::named_bar_sync(1, 128);      // fixbuf reuse
                     }
                 } else if (misc[1]) {
                     __threadfence();
