@@ -229,7 +229,9 @@ def test_gemm_deterministic(fireq):
 
 
 @pytest.mark.parametrize("name,M", [("llama2-7b.gate", 16), ("llama2-7b.down", 16), ("llama3-8b.k", 16),
-                                    ("llama3-8b.down", 16), ("llama2-7b.up", 1024)])
+                                    ("llama3-8b.down", 16), ("llama2-7b.up", 1024),
+                                    # mid-M (C5 sweep): pure stream-K with the bulk-staged owner fixup
+                                    ("llama3-8b.down", 64), ("llama3-8b.down", 128), ("llama3-8b.down", 256)])
 def test_gemm_full_size_sampled(fireq, name, M):
     """BASELINE full shapes in the bench's launch configuration; oracle on sampled channels.
 
