@@ -422,8 +422,32 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
     };
     if (warp == kWProdW) {
         __syncwarp();                          // lane 0's barrier inits precede the issues
-        st.init(a0, blockIdx.x);
-        while (w_issued < w_early && st.next(nt, mt, g, ng, sfirst, slast)) issue_w(a0, w_issued++, pol_w0);
+        // the first segment by a short straight-line computation (this code runs with a cold
+        // instruction cache; the general schedule iterator is several KB of branches)
+        int tile0 = -1, s0 = 0, s1 = 0;
+        const int cta = blockIdx.x;
+        if (a0.S > 1) {
+            const int q = cta % a0.S;
+            tile0 = cta / a0.S; s0 = q * a0.G / a0.S; s1 = (q + 1) * a0.G / a0.S;
+        } else {
+            const unsigned u = a0.U ? (unsigned)cta * a0.U / (unsigned)a0.C : 0u;
+            const unsigned ue = a0.U ? (unsigned)(cta + 1) * a0.U / (unsigned)a0.C : 0u;
+            if (u < ue) {
+                tile0 = (int)(u / (unsigned)a0.G);
+                s0 = (int)(u - (unsigned)tile0 * (unsigned)a0.G);
+                s1 = min(a0.G, s0 + (int)(ue - u));
+            } else if (a0.R + cta < a0.tiles) {
+                tile0 = a0.R + cta; s0 = 0; s1 = a0.G;
+            }
+        }
+        if (tile0 >= 0) {
+            nt = tile0 % a0.n_tiles;
+            for (int q = 0; q < w_early && s0 + q * GPS < s1; ++q) {
+                g = s0 + q * GPS;
+                ng = min(GPS, s1 - g);
+                issue_w(a0, w_issued++, pol_w0);
+            }
+        }
     }
     if (warp == kWAlloc) {
         ptx::tmem_alloc(&misc[0], C::kTmemCols);
@@ -463,7 +487,9 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         for (int ph = 0; ph < NPH; ++ph) {
         const GemmArgs& a = ph ? a1 : a0;
         const uint64_t pol_w = ph == 0 ? pol_w0 : a.m_tiles == 1 ? ptx::policy_evict_first() : ptx::policy_evict_last();
-        if (ph > 0 || w_issued == 0) st.init(a, blockIdx.x);   // phase 0: continue after the early issues
+        st.init(a, blockIdx.x);
+        if (ph == 0)                                        // past the early issues
+            for (int k = 0; k < w_issued; ++k) st.next(nt, mt, g, ng, sfirst, slast);
         while (st.next(nt, mt, g, ng, sfirst, slast)) {
             const int s = i % STAGES;
             ptx::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
