@@ -427,6 +427,8 @@ def run_fireq(args, rank, world, dev):
 
     # ---------------- prefill FFN (FP8 tensor bound) and single-GEMM figures
     del g_multi, g_single, g_gu, g_d
+    chain_info = decode_chain_figures(F, dev, stream, peaks)
+    chain_info["fused_qkv_gate_up"] = decode_chain_figures(F, dev, stream, peaks, fused=True)
     pre_info = prefill_figures(F, dev, stream, peaks) if not args.no_prefill else None
 
     # ---------------- cpu baseline (oracle on a bounded sample)
@@ -457,11 +459,71 @@ def run_fireq(args, rank, world, dev):
         "offline": {"quantize_weight_ms_gate_up_and_down": round(ffn.offline_s * 1e3, 2)},
         "clocks": clocks.summary(),
     }
+    line["decode_chain"] = chain_info
     if pre_info:
         line["prefill"] = pre_info
     if cpu:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
+
+
+def decode_chain_figures(F, dev, stream, peaks, layers=4, fused=False):
+    """SURVEY §8(d) d4 primary decode number (steady state): one CUDA graph of PDL-chained
+    decode GEMMs (M = 16) over DISTINCT weight matrices -- the 7 Llama3-8B linear shapes
+    x 4 layers, 436 MB of packed weights (> 2 x L2) -- GB/s = sum of algorithmic bytes /
+    time.  One layer is quantized from the synthetic generator; the other layers are
+    copies at distinct addresses (values do not change the speed)."""
+    M = M_DECODE
+    shapes = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096),
+              ("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336)]
+    if fused:      # serving-style merged projections: [q; k; v] and [gate; up] as one weight each
+        shapes = [("qkv", 6144, 4096), ("o", 4096, 4096), ("gate_up", 28672, 4096), ("down", 4096, 14336)]
+    xs = {}
+    gemms = []
+    for name, N, K in shapes:
+        W = synth.bits_to_torch(synth.weights(N, K, synth.layer_seed(3, len(gemms)))).to(dev)
+        qw = F.quantize_weight(W, cas_mode=1)
+        n = qw.n
+        del W
+        if K not in xs:
+            X = synth.bits_to_torch(synth.activations(M, K, synth.layer_seed(3, 100 + K % 97))).to(dev)
+            xs[K] = F.quantize_act(X)
+        copies = [(qw.packed, qw.scales)] + [(qw.packed.clone(), qw.scales.clone()) for _ in range(layers - 1)]
+        out = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+        ws = F.Workspace(F.gemm_workspace_bytes(M, N, K), dev)
+        gemms.append((N, K, n, copies, out, ws))
+    torch.cuda.synchronize()
+
+    seq = [(layer, i) for layer in range(layers) for i in range(len(gemms))]
+
+    def chain(prefetch):
+        for j, (layer, i) in enumerate(seq):
+            N, K, n, copies, out, ws = gemms[i]
+            xq, beta = xs[K]
+            p, sc = copies[layer]
+            nl, ni = seq[(j + 1) % len(seq)]
+            nxt = gemms[ni][3][nl] if prefetch else None     # stream the next GEMM's weights into L2
+            F.w4a8_gemm(xq, beta, p, sc, N, n, out=out, workspace=ws, stream=stream, prefetch=nxt)
+
+    nbytes = layers * sum(gemm_bytes(M, N, K) for _, N, K in shapes)
+    res = {"workload": "llama3-8b-decode-linear-chain" + ("-fused-qkv-gate-up" if fused else ""),
+           "tokens": M, "layers": layers,
+           "gemms": layers * len(shapes), "weight_mb": round(nbytes / 1e6, 1),
+           "graph": "PDL-chained fireq_w4a8_gemm launches"}
+    for key, pf in (("plain", False), ("l2_prefetch_next", True)):
+        with torch.cuda.stream(stream):
+            chain(pf)
+        torch.cuda.synchronize()
+        g = capture(lambda: chain(pf), stream)
+        reps = 30
+        ms = time_graphs([g], reps, 3, stream) / reps
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        res[key] = {"us_per_layer": round(ms * 1e3 / layers, 2), "gbs": round(gbs, 1),
+                    "frac": round(gbs / peaks["hbm_gbs"], 4)}
+        del g
+    del gemms, xs
+    torch.cuda.empty_cache()
+    return res
 
 
 def prefill_figures(F, dev, stream, peaks):
