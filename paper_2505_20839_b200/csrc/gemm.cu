@@ -391,19 +391,9 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         if (NPH == 2) ptx::prefetch_tmap(&tmap_x1);
         FIREQ_TRACE_X(9);
     }
-    // Weight stream first: the producer warp issues the first ring's worth of phase 0's weight
-    // loads right after initializing the barriers -- before the LUT build, the TMEM allocation
-    // and the block barrier -- so the DRAM latency of the first stages overlaps the whole setup
-    // (the ring slots are fresh, no empty waits; the loads only touch the W / sigma ring).
     StageIter<GPS> st;
     int nt, mt, g, ng;
     bool sfirst, slast;
-    int w_issued = 0;
-    // (two stages: the TMA engine accepts a 16 KB stage only every ~500 cycles, so a whole ring
-    // issued here would hold the producer warp -- and the block barrier -- for ~2 us)
-    static_assert(STAGES >= 2, "ring");
-    const int w_early = a0.depth < 2 ? 1 : 2;
-    const uint64_t pol_w0 = a0.m_tiles == 1 ? ptx::policy_evict_first() : ptx::policy_evict_last();
     auto issue_w = [&](const GemmArgs& a, int i, uint64_t pol_w) {
         const int s = i % STAGES;
         if (lane == 0) FIREQ_EVT(i, 0);
@@ -420,56 +410,40 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         }
         __syncwarp();
     };
-    if (warp == kWProdW) {
-        __syncwarp();                          // lane 0's barrier inits precede the issues
-        // the first segment by a short straight-line computation (this code runs with a cold
-        // instruction cache; the general schedule iterator is several KB of branches)
-        int tile0 = -1, s0 = 0, s1 = 0;
-        const int cta = blockIdx.x;
-        if (a0.S > 1) {
-            const int q = cta % a0.S;
-            tile0 = cta / a0.S; s0 = q * a0.G / a0.S; s1 = (q + 1) * a0.G / a0.S;
-        } else {
-            const unsigned u = a0.U ? (unsigned)cta * a0.U / (unsigned)a0.C : 0u;
-            const unsigned ue = a0.U ? (unsigned)(cta + 1) * a0.U / (unsigned)a0.C : 0u;
-            if (u < ue) {
-                tile0 = (int)(u / (unsigned)a0.G);
-                s0 = (int)(u - (unsigned)tile0 * (unsigned)a0.G);
-                s1 = min(a0.G, s0 + (int)(ue - u));
-            } else if (a0.R + cta < a0.tiles) {
-                tile0 = a0.R + cta; s0 = 0; s1 = a0.G;
-            }
-        }
-        if (tile0 >= 0) {
-            nt = tile0 % a0.n_tiles;
-            for (int q = 0; q < w_early && s0 + q * GPS < s1; ++q) {
-                g = s0 + q * GPS;
-                ng = min(GPS, s1 - g);
-                issue_w(a0, w_issued++, pol_w0);
-            }
-        }
-    }
     if (warp == kWAlloc) {
         ptx::tmem_alloc(&misc[0], C::kTmemCols);
         ptx::tmem_relinquish();
         if (lane == 0) FIREQ_TRACE_X(10);
     }
-    {
+    // Setup barrier (named barrier 2, all threads).  The weight producer only ARRIVES once its
+    // barrier inits are done and goes straight to streaming: the weights do not depend on the
+    // LUT, the TMEM allocation or the previous kernel, and a blocked TMA issue (the engine takes
+    // a 16 KB stage every ~500 cycles) must not hold the other warps' setup barrier.
+    // (decode tiles only: with the large prefill tiles an immediate full-ring weight stream
+    // delays the first activation tiles, measured 10% slower at M = 128)
+    constexpr bool kStreamFirst = NTOK <= 32;
+    if (kStreamFirst && warp == kWProdW) {
+        __syncwarp();
+        ptx::named_bar_arrive(2, C::kThreads);
+        if (a.S > 1) ptx::cluster_arrive();   // its inits are among those the peers wait for
+    } else {
         // LUT-of-LUTs: entry [s][u] = E4M3_RN(v(u) * sigma_s) for all 127 finite sigma codes
-        // (Step 1's 16-entry table).  v * sigma is exact in fp32.  All threads.
+        // (Step 1's 16-entry table).  v * sigma is exact in fp32.  All warps but a
+        // streaming weight producer.
         uint8_t* lut = reinterpret_cast<uint8_t*>(sLut);
-        for (int e = threadIdx.x; e < kLutEntries; e += C::kThreads) {
+        const int t = (!kStreamFirst || warp < kWProdW) ? (int)threadIdx.x : (int)threadIdx.x - 32;
+        for (int e = t; e < kLutEntries; e += C::kThreads - (kStreamFirst ? 32 : 0)) {
             const int s = e >> 4, u = e & 15;
             const float v = (float)(u < 8 ? u : u - 16);
             lut[e] = (uint8_t)e4m3_rn(__fmul_rn(v, e4m3_decode((uint32_t)s)));
         }
         if (threadIdx.x == 0) FIREQ_TRACE_X(12);
+        ptx::tc_fence_before();
+        ptx::named_bar_sync(2, C::kThreads);
+        ptx::tc_fence_after();
+        if (a.S > 1) ptx::cluster_sync();   // peers' mbarrier inits visible before any st.async
     }
-    ptx::tc_fence_before();
-    __syncthreads();
-    ptx::tc_fence_after();
-    if (a.S > 1) ptx::cluster_sync();       // peers' mbarrier inits visible before any st.async
-    const uint32_t tmem = misc[0];
+    const uint32_t tmem = misc[0];          // (not used by the weight producer)
     if (threadIdx.x == 0) FIREQ_TRACE(1);
     if (threadIdx.x == 0) FIREQ_TRACE_X(13);   // after the barrier is really released: misc[0] read
 
@@ -483,13 +457,11 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         // lane issues (a lane-0 branch makes the compiler wrap TMAs in waterfall loops).
         // decode: weights are streamed once (evict first); prefill: every m-tile re-reads
         // them, so keep them in L2 (the 126 MB L2 holds the largest layer's weights)
-        int i = w_issued;
+        int i = 0;
         for (int ph = 0; ph < NPH; ++ph) {
         const GemmArgs& a = ph ? a1 : a0;
-        const uint64_t pol_w = ph == 0 ? pol_w0 : a.m_tiles == 1 ? ptx::policy_evict_first() : ptx::policy_evict_last();
+        const uint64_t pol_w = a.m_tiles == 1 ? ptx::policy_evict_first() : ptx::policy_evict_last();
         st.init(a, blockIdx.x);
-        if (ph == 0)                                        // past the early issues
-            for (int k = 0; k < w_issued; ++k) st.next(nt, mt, g, ng, sfirst, slast);
         while (st.next(nt, mt, g, ng, sfirst, slast)) {
             const int s = i % STAGES;
             ptx::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
