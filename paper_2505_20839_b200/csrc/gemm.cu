@@ -320,7 +320,9 @@ __device__ __forceinline__ void conv_mask_select(uint32_t w, uint32_t L0, uint32
 __device__ __forceinline__ float div_for_e4m3(float x, float beta, float rcp) {
     const float q0 = __fmul_rn(x, rcp);
     const float e = __fmaf_rn(-q0, beta, x);
-    return __fmaf_rn(e, rcp, q0);
+    // x = -0: the correction's +0 would lose the sign; OR-ing x's sign bit is a no-op otherwise
+    // (beta > 0, so a nonzero or underflowed quotient already carries x's sign)
+    return __int_as_float(__float_as_int(__fmaf_rn(e, rcp, q0)) | (__float_as_int(x) & 0x80000000));
 }
 
 // Roles (warp-uniform, see kW* below): converter warpgroups, epilogue warpgroup, TMEM

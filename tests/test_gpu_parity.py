@@ -125,6 +125,29 @@ def test_quantize_act(fireq, M, K, with_c):
     assert np.array_equal(xq.cpu().numpy(), rq)
 
 
+def test_quantize_act_exhaustive_bf16(fireq):
+    """Every finite bf16 x' below the row amax, for several amax values (so beta = bf16(amax/448)
+    spans exponents and mantissas): the reciprocal + residual-FMA quotient of the GPU encode
+    must give the oracle's E4M3 codes bit-exactly (DESIGN reading R22)."""
+    pos = np.arange(0x0000, 0x7F80, dtype=np.uint32)            # all finite non-negative bf16 patterns
+    vals = (pos << 16).astype(np.uint32).view(np.float32).astype(np.float64)
+    amaxes = [448.0, 1.0, 3.140625, 0.0078125 * 1.5, 2.0 ** -100 * 1.75, 57344.0, 1.0e30]
+    rows = []
+    for A in amaxes:
+        A = float(nm.bf16_rn(np.array([A]))[0])
+        v = vals[vals <= A]
+        rows.append(np.concatenate([v, -v, [A]]))
+    K = (max(len(r) for r in rows) + 127) // 128 * 128
+    X = np.zeros((len(rows), K))
+    for i, r in enumerate(rows):
+        X[i, : len(r)] = r
+    xb = nm.bf16_to_bits(X)
+    xq, beta = fireq.quantize_act(to_dev_bf16(xb))
+    rq, rbeta = oq.quantize_act(X)
+    assert np.array_equal(bits_of(beta), nm.bf16_to_bits(rbeta))
+    assert np.array_equal(xq.cpu().numpy(), rq)
+
+
 def test_quantize_act_strided(fireq):
     M, K, ld = 8, 256, 384
     xb = synth.activations(M, ld, 77)
