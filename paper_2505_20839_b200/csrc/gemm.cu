@@ -63,6 +63,8 @@ struct GemmArgs {
     int R;                 // tiles [0, R) are split contiguously over CTAs ("stream-K")
     int C;                 // CTAs in the grid
     unsigned U;            // stream-K units = R * G (< 2^31: R < 2 * SMs, G <= K / 128)
+    unsigned Cs;           // CTAs sharing the U units: min(C, U), so every sharer has >= 1 unit
+                           // (a contributor with an empty range would never publish its partial)
     int S;                 // > 1: cluster split-K, one tile per cluster of S CTAs (K split S ways)
     int depth;             // weight stages in flight (<= STAGES): bounds the loaded HBM latency
     // out_layout 2 (SwiGLU pairs): tile rows [0, 64) are gate channels j0 + r, rows [64, 128)
@@ -119,6 +121,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define FIREQ_TRACE2(slot) do { } while (0)
 #endif
 
+// First stream-K unit of CTA c: the U units are split contiguously over the first Cs CTAs.
+__device__ __forceinline__ unsigned split_begin(unsigned c, unsigned U, unsigned Cs) {
+    return c >= Cs ? U : c * U / Cs;
+}
+
 // Segment = contiguous run of groups [g0, g1) of one tile processed by one CTA.
 // Schedule of CTA c: first its share [c*U/C, (c+1)*U/C) of the stream-K units of tiles
 // [0, R) (so that split tiles are reduced early, overlapped with later work), then the
@@ -128,8 +135,8 @@ struct SegIter {
     unsigned u, u_end;     // 32-bit schedule math: 64-bit division is a slow called routine
     __device__ __forceinline__ void init(const GemmArgs& a, int cta) {
         G = a.G; tiles = a.tiles; C = a.C; c = cta; R = a.R; k = 0; S = a.S;
-        u = a.U ? (unsigned)cta * a.U / (unsigned)a.C : 0u;
-        u_end = a.U ? (unsigned)(cta + 1) * a.U / (unsigned)a.C : 0u;
+        u = split_begin((unsigned)cta, a.U, a.Cs);
+        u_end = split_begin((unsigned)cta + 1u, a.U, a.Cs);
     }
     __device__ __forceinline__ bool next(int& tile, int& g0, int& g1) {
         if (S > 1) {
@@ -706,7 +713,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         const GemmArgs& a = ph ? a1 : a0;
         const float p2 = exp2_neg(a.pts_n);
         it.init(a, blockIdx.x);
-        const unsigned u_first = blockIdx.x * a.U / (unsigned)a.C;
+        const unsigned u_first = split_begin(blockIdx.x, a.U, a.Cs);
         int ntile = 0, m0 = 0, n = 0;
         float gam = 1.0f;
         const bool use_gam = a.gamma != nullptr || (a.out_layout == 2 && a.gamma_up != nullptr);
@@ -799,7 +806,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             // stream-K tile: contributors c_lo..c_hi in CTA order; c_lo (for which this tile is
             // its LAST split segment, so the others published long ago) reduces it
             const unsigned t0 = (unsigned)tile * (unsigned)a.G, t1 = t0 + (unsigned)a.G - 1u;
-            const int c_lo = whole ? 0 : owner_of(t0, a.U, a.C), c_hi = whole ? 0 : owner_of(t1, a.U, a.C);
+            const int c_lo = whole ? 0 : owner_of(t0, a.U, (int)a.Cs), c_hi = whole ? 0 : owner_of(t1, a.U, (int)a.Cs);
             const bool owner = !whole && (int)blockIdx.x == c_lo;
             const bool keep_own = owner && C::kFixSlots > 0;      // own partial stays in registers
             float own[C::kFixSlots > 0 ? NTOK : 1];
@@ -925,7 +932,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                             ptx::mbar_arrive_expect_tx(fixbar, nb * C::kPartBytes);
                             for (int q = 0; q < nb; ++q) {
                                 const int cc = cc0 + q;
-                                const unsigned cu0 = (unsigned)cc * a.U / (unsigned)a.C;
+                                const unsigned cu0 = split_begin((unsigned)cc, a.U, a.Cs);
                                 const int sl = 2 * cc + ((cu0 < t0) ? 1 : 0);
                                 ptx::bulk_g2s(fixbuf + q * (C::kPartBytes / 4), a.partial + (size_t)sl * NTOK * kTileN,
                                               C::kPartBytes, fixbar, 0ull);
@@ -964,7 +971,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                             ptx::mbar_arrive_expect_tx(fixbar, (uint32_t)(nb * kPart * 4));
                             for (int q = 0; q < nb; ++q) {
                                 const int cc = cc0 + q;
-                                const unsigned cu0 = (unsigned)cc * a.U / (unsigned)a.C;
+                                const unsigned cu0 = split_begin((unsigned)cc, a.U, a.Cs);
                                 const int sl = 2 * cc + ((cu0 < t0) ? 1 : 0);
                                 ptx::bulk_g2s(fixbuf + q * kPart, a.partial + (size_t)sl * kPart, kPart * 4, fixbar, 0ull);
                             }
@@ -1013,7 +1020,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                             for (int q = 0; q < 4; ++q) {
                                 const int cc = cc0 + q;
                                 if (cc <= c_hi) {
-                                    const unsigned cu0 = (unsigned)cc * a.U / (unsigned)a.C;
+                                    const unsigned cu0 = split_begin((unsigned)cc, a.U, a.Cs);
                                     const int sl = 2 * cc + ((cu0 < t0) ? 1 : 0);
                                     const float* pp = a.partial + (size_t)sl * NTOK * kTileN;
 #pragma unroll
@@ -1195,13 +1202,17 @@ bool make_x_map(CUtensorMap* out, const uint8_t* x, int64_t M, int64_t K, int nt
 
 struct Plan {
     int ntok, m_tiles, n_tiles, tiles, G, mode, C, R, S;
+    int Cs;                // CTAs sharing the stream-K units
     long long U;
     bool sign_split;
 };
 
 Plan make_plan(int64_t M, int64_t N, int64_t K, bool allow_cluster = true) {
     Plan p{};
-    p.ntok = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 192;
+    // prefill: 224 tokens per tile (2 x 224 accumulator columns + 2 converted A stages fill
+    // TMEM; 14% fewer conversions per MAC than 192, measured 6-8% faster at M = 16384); 192
+    // below 2048 tokens, where the coarser m-tile padding costs more
+    p.ntok = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : M < 2048 ? 192 : 224;
     p.sign_split = p.ntok <= 128;
     p.m_tiles = (int)((M + p.ntok - 1) / p.ntok);
     p.n_tiles = (int)(N / kTileN);
@@ -1220,6 +1231,10 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, bool allow_cluster = true) {
     }
     p.U = (long long)p.R * p.G;
     p.mode = p.R > 0 ? 1 : 0;
+    // sharers of the split units: every sharer needs >= 1 unit; with large token tiles
+    // (NTOK > 32: 32-112 KB FP32 partials through L2) at most 4 contributors per split tile
+    p.Cs = (int)std::min<long long>(p.C, p.U);
+    if (p.ntok > 32 && p.R > 0 && p.tiles >= sms) p.Cs = std::min(p.Cs, 4 * p.R);   // hybrid only
     p.S = 1;
     // Few tiles (decode-sized N): split K over a cluster of S CTAs per tile and reduce the
     // partials through DSMEM instead of stream-K's global-memory fixup (no second round trip
@@ -1233,6 +1248,7 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, bool allow_cluster = true) {
             p.mode = 2;
             p.R = 0;
             p.U = 0;
+            p.Cs = 0;
             p.C = p.tiles * S;
         }
     }
@@ -1298,6 +1314,7 @@ GemmArgs base_args(const Plan& p, int64_t M, int64_t N, int64_t K, const uint8_t
     args.R = p.R;
     args.C = p.C;
     args.U = (unsigned)p.U;
+    args.Cs = (unsigned)p.Cs;
     args.S = p.S;
     {
         static const int depth = getenv("FIREQ_DEPTH") ? atoi(getenv("FIREQ_DEPTH")) : 1000;   // experiments
@@ -1349,6 +1366,7 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
         case 32:  return launch_cfg<32, true, 3, 7, 3, 2, 2, 1>(map, args, stream);
         case 64:  return launch_cfg<64, true, 2, 5, 2, 2, 2, 1>(map, args, stream);
         case 128: return launch_cfg<128, true, 2, 7, 4, 2, 1, 1>(map, args, stream);
+        case 224: return launch_cfg<224, false, 2, 5, 2, 2, 1, 1>(map, args, stream);   // TMEM 448 + 64
         default:  return launch_cfg<192, false, 2, 6, 4, 2, 1, 1>(map, args, stream);
     }
 }

@@ -186,6 +186,7 @@ def run_case(fireq, M, N, K, cas=1, gamma=False, out_layout=0, seed=0):
     (1, 128, 128), (7, 256, 512), (16, 512, 1024), (16, 1024, 4096), (17, 384, 640), (32, 256, 2048),
     (64, 640, 1024), (100, 256, 768), (128, 512, 512), (129, 256, 1024), (256, 384, 512), (300, 256, 384),
     (513, 128, 256),
+    (2100, 256, 512), (4096, 384, 256),          # prefill tiles of 224 tokens, ragged last m-tile
 ])
 def test_gemm_g4(fireq, M, N, K):
     y, r, *_ = run_case(fireq, M, N, K, seed=M * 131 + N + K)
@@ -205,6 +206,18 @@ def test_gemm_schedules(fireq, M, N, K, mode):
     plan = fireq.gemm_plan(M, N, K)
     assert plan["mode"] == mode, plan          # schedules as chosen on a 148-SM B200
     y, r, *_ = run_case(fireq, M, N, K, seed=N + K)
+    assert og.g4_error(y, r) <= G4_TOL
+    assert og.rel_frobenius(y, r) < 5e-3
+
+
+@pytest.mark.parametrize("M,N,K", [(16, 150 * 128, 512), (200, 75 * 128, 512)])
+def test_gemm_hybrid_few_remainder_units(fireq, M, N, K):
+    """Whole tiles for one full wave plus a remainder of 2 tiles whose 8 K-units are fewer than
+    the CTAs: the units are shared by 8 CTAs only (a sharer without units would never publish
+    its partial and the tile's owner would wait forever)."""
+    plan = fireq.gemm_plan(M, N, K)
+    assert plan["mode"] == "stream-k" and plan["ctas"] == 148, plan
+    y, r, *_ = run_case(fireq, M, N, K, seed=N + M)
     assert og.g4_error(y, r) <= G4_TOL
     assert og.rel_frobenius(y, r) < 5e-3
 
@@ -254,7 +267,8 @@ def test_gemm_deterministic(fireq):
 @pytest.mark.parametrize("name,M", [("llama2-7b.gate", 16), ("llama2-7b.down", 16), ("llama3-8b.k", 16),
                                     ("llama3-8b.down", 16), ("llama2-7b.up", 1024),
                                     # mid-M (C5 sweep): pure stream-K with the bulk-staged owner fixup
-                                    ("llama3-8b.down", 64), ("llama3-8b.down", 128), ("llama3-8b.down", 256)])
+                                    ("llama3-8b.down", 64), ("llama3-8b.down", 128), ("llama3-8b.down", 256),
+                                    ("llama3-8b.k", 4096)])
 def test_gemm_full_size_sampled(fireq, name, M):
     """BASELINE full shapes in the bench's launch configuration; oracle on sampled channels.
 
