@@ -1210,9 +1210,10 @@ struct Plan {
 Plan make_plan(int64_t M, int64_t N, int64_t K, bool allow_cluster = true) {
     Plan p{};
     // prefill: 224 tokens per tile (2 x 224 accumulator columns + 2 converted A stages fill
-    // TMEM; 14% fewer conversions per MAC than 192, measured 6-8% faster at M = 16384); 192
-    // below 2048 tokens, where the coarser m-tile padding costs more
-    p.ntok = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : M < 2048 ? 192 : 224;
+    // TMEM; 14% fewer conversions per MAC than 192, measured 6-8% faster at M = 16384) unless
+    // its coarser m-tile padding costs > 5% more MMA work than 192-token tiles
+    p.ntok = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 192;
+    if (M > 128 && 224 * ((M + 223) / 224) * 100 <= 105 * 192 * ((M + 191) / 192)) p.ntok = 224;
     p.sign_split = p.ntok <= 128;
     p.m_tiles = (int)((M + p.ntok - 1) / p.ntok);
     p.n_tiles = (int)(N / kTileN);

@@ -210,7 +210,7 @@ def test_gemm_schedules(fireq, M, N, K, mode):
     assert og.rel_frobenius(y, r) < 5e-3
 
 
-@pytest.mark.parametrize("M,N,K", [(16, 150 * 128, 512), (200, 75 * 128, 512)])
+@pytest.mark.parametrize("M,N,K", [(16, 150 * 128, 512), (300, 75 * 128, 512)])
 def test_gemm_hybrid_few_remainder_units(fireq, M, N, K):
     """Whole tiles for one full wave plus a remainder of 2 tiles whose 8 K-units are fewer than
     the CTAs: the units are shared by 8 CTAs only (a sharer without units would never publish
