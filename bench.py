@@ -345,7 +345,7 @@ def run_fireq(args, rank, world, dev):
     stream = torch.cuda.Stream(device=dev)
     if world > 1 or args.colpar:
         from paper_2505_20839_b200 import multigpu
-        return multigpu.run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src)
+        return multigpu.run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src, clock_cls=ClockSampler)
 
     # ---------------- decode FFN (headline): quantize_act, gemm, silu_mul_quantize_act, gemm
     ffn = FFN(F, M_DECODE, ROTATIONS, dev)

@@ -27,7 +27,7 @@ from . import sharding
 D_MODEL, D_FF = 4096, 11008
 
 
-def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src):
+def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src, clock_cls=None):
     import synth
     M = 16
     R = 4
@@ -98,6 +98,17 @@ def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src):
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
+    clocks = clock_cls(dev.index or 0) if (clock_cls is not None and rank == 0) else None
+    if clocks:
+        # a longer pass under the clock sampler (nvidia-smi polls every ~0.1 s), then the timed K
+        clocks.start()
+        time.sleep(0.25)
+        with torch.cuda.stream(stream):
+            for _ in range(max(calls, 20000 // per_call)):
+                replay()
+        torch.cuda.synchronize()
+        clocks.stop()
+    dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         e0.record(stream)
@@ -109,6 +120,33 @@ def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src):
     ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     us_per_step = float(ms.item()) * 1e3 / steps
+
+    # end to end through host buffers: pinned H2D of x and D2H of the gathered y every step
+    x_host = x.cpu().pin_memory()
+    y_host = torch.empty_like(yt, device="cpu").pin_memory()
+
+    def e2e_step(r):
+        x.copy_(x_host, non_blocking=True)
+        step(r)
+        y_host.copy_(yt, non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        for r in range(R):
+            e2e_step(r)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e2.record(stream)
+        for i in range(steps):
+            e2e_step(i % R)
+        e3.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms2 = torch.tensor([e2.elapsed_time(e3)], device=dev)
+    dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
+    e2e_us = float(ms2.item()) * 1e3 / steps
     comm.destroy()
     if rank == 0:
         line = {
@@ -120,5 +158,9 @@ def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src):
                        "parallelism": f"column-parallel tp{world} (N-sharded gate_up + down, NCCL all-gather of Y^T)",
                        "l2": f"{R} rotating weight-shard copies", "graph": "captured" if graphed else "eager"},
             "gpu_launches": 4 * steps,
+            "e2e": {"value": round(e2e_us, 3), "unit": "us", "h2d_bytes_per_step": x.numel() * 2,
+                    "d2h_bytes_per_step": yt.numel() * 2, "timing": "eager launches, max over ranks"},
         }
+        if clocks:
+            line["clocks"] = clocks.summary()
         print(json.dumps(line), flush=True)
