@@ -148,6 +148,36 @@ def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src, clock_c
     dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
     e2e_us = float(ms2.item()) * 1e3 / steps
     comm.destroy()
+
+    # dominant kernel: this rank's gate_up shard GEMM alone (no collective), rotating copies
+    gu_out = torch.empty((M, plan_gu.N_local), dtype=torch.bfloat16, device=dev)
+
+    def gu_only(r):
+        pg, sg, _, _ = rot[r]
+        F.w4a8_gemm(xq, beta, pg, sg, plan_gu.N_local, n_gu, gamma=gamma_l, out=gu_out, workspace=ws1, stream=stream)
+
+    with torch.cuda.stream(stream):
+        for r in range(R):
+            gu_only(r)
+    torch.cuda.synchronize()
+    g_gu = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_gu, stream=stream):
+        for r in range(R):
+            gu_only(r)
+    with torch.cuda.stream(stream):
+        g_gu.replay()
+    torch.cuda.synchronize()
+    e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 50
+    with torch.cuda.stream(stream):
+        e4.record(stream)
+        for _ in range(reps):
+            g_gu.replay()
+        e5.record(stream)
+    torch.cuda.synchronize()
+    gu_us = e4.elapsed_time(e5) * 1e3 / (reps * R)
+    Nl = plan_gu.N_local
+    gu_bytes = Nl * D_MODEL // 2 + Nl * D_MODEL // 128 + M * D_MODEL + 2 * M + 2 * M * Nl
     if rank == 0:
         line = {
             "metric": "Llama2-7B FFN latency at batch 16 (W4A8-FP: INT4 weights + FP8 g128 scales, FP8 activations)",
@@ -163,4 +193,10 @@ def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src, clock_c
         }
         if clocks:
             line["clocks"] = clocks.summary()
+        hbm = peaks["hbm_gbs"]
+        line["roofline"] = {"bound": "hbm", "kernel": f"fireq_w4a8_gemm gate_up shard M={M} N={Nl} K={D_MODEL} (per rank)",
+                            "achieved": round(gu_bytes / gu_us / 1e3, 1), "peak": hbm, "unit": "GB/s",
+                            "frac": round(gu_bytes / gu_us / 1e3 / hbm, 4), "traffic": None,
+                            "algorithmic_bytes": gu_bytes, "launch_us": round(gu_us, 3),
+                            "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
         print(json.dumps(line), flush=True)
