@@ -29,6 +29,13 @@
  *     launch failed (FIREQ_ERROR_CUDA); fireq_last_error() then returns a
  *     thread-local human-readable detail.
  *   - Row-major everywhere; "ld*" are leading dimensions in elements.
+ *   - Some GEMM schedules (stream-K remainders, the fused FFN) have CTAs wait on
+ *     other CTAs of the same grid; those grids are at most one CTA per SM and rely
+ *     on all their CTAs being resident together (as CUTLASS's stream-K does).  Do
+ *     not run them concurrently with a kernel that holds SMs for its whole
+ *     duration, or set FIREQ_COOPERATIVE=1 in the environment: such grids are then
+ *     launched cooperatively (guaranteed co-residency; the launch fails rather than
+ *     hangs; ~1.4 us slower per launch).
  */
 #ifndef FIREQ_H_
 #define FIREQ_H_
@@ -55,6 +62,12 @@ typedef enum {
 const char* fireq_status_string(fireq_status_t status);
 /* Detail of the last failing call on this host thread ("" if none). */
 const char* fireq_last_error(void);
+
+/* Drops the library's cached TMA descriptors (keyed by activation pointer, shape
+ * and tile; they embed device addresses).  Call after freeing activation buffers
+ * that may be reallocated at the same address with different contents layout, or
+ * before cudaDeviceReset.  Host-only, thread-safe. */
+void fireq_clear_cache(void);
 
 /* Version of the packed weight layout produced by fireq_quantize_weight
  * (currently 1). */
@@ -166,7 +179,8 @@ fireq_status_t fireq_silu_mul_quantize_act_t(const void* Gt, const void* Ut, int
  *   pts_exponent host int n in [0, 60] (pts_and_status[0]).
  *   out_chan_scale  float [N] gamma or NULL.
  *   Y            out bf16: out_layout 0 -> Y[M][ldy] (ldy >= N), 1 -> Y^T [N][ldy]
- *                (ldy >= M).  ldy % 8 == 0, 16-B aligned.  Rows/cols outside
+ *                (ldy >= M).  16-B aligned; ldy % 8 == 0 for layout 0 (any ldy >= M
+                for Y^T; 16-B vector stores when ldy % 8 == 0).  Rows/cols outside
  *                [0,M) x [0,N) are never written.
  *   workspace    >= fireq_w4a8_gemm_workspace_bytes(M, N, K) (see there).
  */
@@ -212,9 +226,10 @@ fireq_status_t fireq_comm_destroy(fireq_comm_t comm);
  * may end in zero-padded rows so that all shards have equal N_local, a multiple
  * of 128).  X is replicated.  The rank computes its slice with fireq_w4a8_gemm in
  * the Y^T layout directly into its slot of Yt_full [N_local*nranks][M] and an
- * in-place ncclAllGather (bf16) over NVLink completes Y^T on every rank, on `stream`.
+ * in-place ncclAllGather (bf16) over NVLink completes Y^T on every rank, on `stream`
+ * (also at nranks == 1, where it is a no-op copy).
  *   out_chan_scale_local  float [N_local] gamma for this shard's rows, or NULL.
- *   Yt_full   out bf16 [nranks*N_local][M] (Y^T, ld = M; M % 8 == 0).
+ *   Yt_full   out bf16 [nranks*N_local][M] (Y^T, ld = M; any M >= 1).
  */
 fireq_status_t fireq_w4a8_gemm_colpar(const uint8_t* x_fp8, const void* x_scale, int64_t M,
                                       int64_t K, const uint8_t* w_packed_local,
@@ -228,7 +243,8 @@ fireq_status_t fireq_w4a8_gemm_colpar(const uint8_t* x_fp8, const void* x_scale,
  * (entry [s][u] = E4M3_RN(v(u) * dec(s)), v(u) = u < 8 ? u : u - 16) into the
  * device buffer out[2032], on `stream`. */
 fireq_status_t fireq_debug_lut_table(uint8_t* out, void* stream);
-/* Debug/profiling: when buf != NULL, every later fireq_w4a8_gemm launch records a
+/* Debug/profiling (profile builds only; no-op otherwise): when buf != NULL, every
+ * later fireq_w4a8_gemm launch records a
  * per-CTA %globaltimer timeline into the device buffer buf ([ctas][8] uint64:
  * start, setup done, first stage landed, MMA issue done, epilogue done, end).
  * Pass NULL to disable.  Not thread-safe; for benchmarks only. */

@@ -163,10 +163,13 @@ class QuantizedWeight:
         self.__dict__.update(kw)
 
 
-def quantize_weight(W, cas_mode, pack=True):
+def quantize_weight(W, cas_mode, pack=True, rows=None):
     """W1-W6 for a bf16 weight matrix W [N][K] (float64 array of bf16 values).
 
     pack=False skips W6 (packed/scales are None) for large sampled checks.
+    rows (with pack=False): W4-W5 only for those output rows -- CAS (W1) and PTS (W3)
+    are still computed over the whole tensor, as their definitions require; W4-W5 act
+    on each row independently, so sigma/codes of a row do not depend on the others.
 
     Returns QuantizedWeight with: lam (fp32 values), c (bf16 values),
     n (PTS exponent), reason, sigma [N][G] (values), sigma_codes [N][G],
@@ -181,6 +184,10 @@ def quantize_weight(W, cas_mode, pack=True):
     lam, c = cas_lambda(W, cas_mode)
     W_bar = cas_apply(W, lam)
     n, reason = pts_exponent(W_bar)
+    if rows is not None:
+        if pack:
+            raise ValueError("rows= needs pack=False")
+        W_bar = W_bar[np.asarray(rows)]
     W_tilde = W_bar * 2.0 ** n                     # exact power-of-two scaling
     sigma, codes = quantize_groups(W_tilde)
     sigma_codes = e4m3_encode(sigma)

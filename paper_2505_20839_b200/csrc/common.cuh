@@ -19,16 +19,17 @@ int max_smem_optin();
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-// Launch with programmatic stream serialization (PDL) and an optional cluster shape.
+// Launch with programmatic stream serialization (PDL), an optional cluster shape and,
+// for grids whose CTAs wait on each other, the cooperative attribute (all CTAs resident).
 template <typename Kern, typename... Args>
 cudaError_t launch_ex(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, unsigned cluster_x,
-                      Args... args) {
+                      bool cooperative, Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attrs[2];
+    cudaLaunchAttribute attrs[3];
     unsigned n = 0;
     attrs[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attrs[n].val.programmaticStreamSerializationAllowed = 1;
@@ -38,6 +39,11 @@ cudaError_t launch_ex(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_
         attrs[n].val.clusterDim.x = cluster_x;
         attrs[n].val.clusterDim.y = 1;
         attrs[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    if (cooperative) {
+        attrs[n].id = cudaLaunchAttributeCooperative;
+        attrs[n].val.cooperative = 1;
         ++n;
     }
     cfg.attrs = attrs;

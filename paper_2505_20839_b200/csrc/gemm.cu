@@ -46,6 +46,7 @@ constexpr int kGroup = 128;            // K per group (one FP8 scale)
 constexpr int kTileN = 128;            // weight rows per tile = MMA M
 constexpr int kWBytes = kTileN * kGroup / 2;   // 8192 packed bytes per (tile, group)
 constexpr int kLutEntries = 127 * 16;
+constexpr int kMaxDevices = 64;
 
 struct GemmArgs {
     const uint8_t* w_packed;
@@ -250,8 +251,9 @@ struct Cfg {
     static constexpr int kOffS = kOffW + STAGES * kWStage;
     static constexpr int kOffLut = kOffS + STAGES * kSStage;
     static constexpr int kOffFix = kOffLut + 2048;
-    static constexpr int kOffEpi = kOffFix + kFixSlots * kPartBytes;    // scales [NTOK] + 4 KB transpose
-    static constexpr int kOffBar = kOffEpi + 1024 + 16 * kTileN * 2;
+    // per-token scales, double-buffered by segment parity (2 x 256 floats) + 4 KB transpose
+    static constexpr int kOffEpi = kOffFix + kFixSlots * kPartBytes;
+    static constexpr int kOffBar = kOffEpi + 2048 + 16 * kTileN * 2;
     static constexpr int kNumBars = 3 * STAGES + 2 * ASTAGES + 2 * ACCBUF + 2;
     static constexpr int kOffMisc = kOffBar + kNumBars * 8;
     static constexpr int kSmemBytes = kOffMisc + 64 + 1024;             // + alignment slack
@@ -325,6 +327,7 @@ __device__ __forceinline__ void conv_mask_select(uint32_t w, uint32_t L0, uint32
 // midpoint lies > 2^-13 relative away from every midpoint, so the E4M3 rounding equals
 // that of the correctly rounded quotient (reading R23).
 __device__ __forceinline__ float div_for_e4m3(float x, float beta, float rcp) {
+    if (beta < 0x1p-126f) return __fdiv_rn(x, beta);   // subnormal beta: 1/beta may overflow
     const float q0 = __fmul_rn(x, rcp);
     const float e = __fmaf_rn(-q0, beta, x);
     // x = -0: the correction's +0 would lose the sign; OR-ing x's sign bit is a no-op otherwise
@@ -408,7 +411,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         if (lane == 0) FIREQ_EVT(i, 0);
         if (lane == 0 && i == 0) FIREQ_TRACE(8);
         if (ptx::elect_one()) {
-            if (a.dbg & 4) {
+            if (FIREQ_PROFILE && (a.dbg & 4)) {
                 ptx::mbar_arrive(&fullW[s]);
             } else {
                 ptx::mbar_arrive_expect_tx(&fullW[s], ng * (kWBytes + kTileN));
@@ -551,6 +554,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         uint32_t d = tmem;
         bool touched = false;
         bool a_ready = false;    // afull of stage i already seen complete by the previous stage's probe
+        bool p1_seen = false;
         long long w_afull = 0, w_full = 0, t_issue = 0, t_mma0 = prof_clock();
         for (int ph = 0; ph < NPH; ++ph) {
         const GemmArgs& a = ph ? a1 : a0;
@@ -567,6 +571,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                 const long long c0 = prof_clock();
                 if (!a_ready) ptx::mbar_wait(&afull[as], (i / ASTAGES) & 1);
                 if (lane == 0) FIREQ_EVT(i, 4);
+                if (NPH == 2 && ph == 1 && lane == 0 && !p1_seen) { p1_seen = true; FIREQ_TRACE2(14); }
                 const long long c1 = prof_clock();
                 if (!C::kFoldX) ptx::mbar_wait(&fullX[s], (i / STAGES) & 1);
                 if (lane == 0) FIREQ_EVT(i, 5);
@@ -581,7 +586,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                 const bool nxt = NMMA == 1 && C::kFoldX &&
                                  ptx::mbar_test_wait(&afull[(i + 1) % ASTAGES], ((i + 1) / ASTAGES) & 1);
                 if (ptx::elect_one()) {
-                    if (!(a.dbg & 2)) {
+                    if (!(FIREQ_PROFILE && (a.dbg & 2))) {
                         for (int q = 0; q < ng; ++q) {
                             const uint64_t bdesc = smem_desc_sw128(sx0 + s * C::kXStage + q * C::kXBytes);
 #pragma unroll
@@ -655,7 +660,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             cw_aempty += prof_clock() - c1;
             if (r == 0) FIREQ_EVT(i, 2);
             ptx::tc_fence_after();
-            if (!(a.dbg & 1)) {
+            if (!(FIREQ_PROFILE && (a.dbg & 1))) {
                 const uint32_t ta = tmem + lane_base + C::kACol0 + as * C::kASz;
 #pragma unroll
                 for (int q = 0; q < GPS; ++q) {
@@ -705,8 +710,12 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         ptx::pdl_wait();                    // beta, workspace and Y are shared with earlier kernels
         const int r = threadIdx.x & 127;
         const uint32_t lane_base = (uint32_t)(r & ~31) << 16;
-        float* sScale = reinterpret_cast<float*>(smem + C::kOffEpi);                 // [NTOK]
-        __nv_bfloat16* sT = reinterpret_cast<__nv_bfloat16*>(smem + C::kOffEpi + 1024);  // [16][128]
+        // [2][256]: segment sg uses buffer sg & 1, so a warp that runs ahead into the next
+        // segment never overwrites scales another warp of this one still reads (the Y^T emit
+        // has no barrier between segments)
+        float* const sScaleBuf = reinterpret_cast<float*>(smem + C::kOffEpi);
+        float* sScale = sScaleBuf;
+        __nv_bfloat16* sT = reinterpret_cast<__nv_bfloat16*>(smem + C::kOffEpi + 2048);  // [16][128]
         int sg = 0, i_stage = 0;
         uint32_t fix_phase = 0;
         for (int ph = 0; ph < NPH; ++ph) {
@@ -732,7 +741,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             const int mb = m0 + ch * 16;
             if (a.out_layout == 1) {
                 __nv_bfloat16* dst = a.Y + (size_t)n * a.ldy + mb;
-                if (mb + 16 <= a.M) {
+                if (mb + 16 <= a.M && (a.ldy & 7) == 0) {
                     reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<const uint4*>(yb)[0];
                     reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<const uint4*>(yb)[1];
                 } else {
@@ -792,6 +801,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                 gam = (r < 64 || !a.gamma_up) ? 1.0f : __bfloat162float(a.gamma_up[ntile * 64 + (r - 64)]);
             else
                 gam = a.gamma ? a.gamma[n] : 1.0f;
+            sScale = sScaleBuf + (sg & 1) * 256;
             for (int t = r; t < NTOK; t += 128)
                 sScale[t] = (m0 + t < a.M) ? __fmul_rn(__bfloat162float(a.x_scale[m0 + t]), p2) : 0.0f;
             const bool csplit = a.S > 1;
@@ -920,7 +930,9 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                     SegIter peek = it;
                     int pt, pg0, pg1;
-                    const bool last_seg = !peek.next(pt, pg0, pg1);
+                    // the weight ring is idle only after the last phase's last segment (with
+                    // NPH = 2 the producer streams phase 1's weights into it meanwhile)
+                    const bool last_seg = !peek.next(pt, pg0, pg1) && (NPH == 1 || ph == NPH - 1);
                     float* fixbuf = last_seg ? reinterpret_cast<float*>(sW) : sFix;
                     const int slots = last_seg ? (STAGES * C::kWStage) / C::kPartBytes : C::kFixSlots;
                     float accv[C::kFixSlots > 0 ? NTOK : 1];
@@ -1128,6 +1140,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                         if (seen < gridDim.x) __nanosleep(64);
                     } while (seen < gridDim.x);
                     ptx::mbar_arrive(ph1bar);       // release to this CTA's activation producer
+                    FIREQ_TRACE2(13);
                     unsigned prev;
                     asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a.bar + 3) : "memory");
                     if (prev == gridDim.x - 1) {    // everyone has passed: reset for the next launch
@@ -1178,10 +1191,20 @@ PFN_encodeTiled get_encode() {
 }
 
 // TMA descriptor cache keyed by (pointer, M, K, box rows).
-bool make_x_map(CUtensorMap* out, const uint8_t* x, int64_t M, int64_t K, int ntok) {
+using XMapCache = std::map<std::tuple<const void*, int64_t, int64_t, int>, CUtensorMap>;
+}  // namespace
+std::mutex& x_map_mu() {
     static std::mutex mu;
-    static std::map<std::tuple<const void*, int64_t, int64_t, int>, CUtensorMap> cache;
-    std::lock_guard<std::mutex> lock(mu);
+    return mu;
+}
+XMapCache& x_map_cache() {
+    static XMapCache cache;
+    return cache;
+}
+namespace {
+bool make_x_map(CUtensorMap* out, const uint8_t* x, int64_t M, int64_t K, int ntok) {
+    XMapCache& cache = x_map_cache();
+    std::lock_guard<std::mutex> lock(x_map_mu());
     auto key = std::make_tuple((const void*)x, M, K, ntok);
     auto itc = cache.find(key);
     if (itc != cache.end()) { *out = itc->second; return true; }
@@ -1199,6 +1222,15 @@ bool make_x_map(CUtensorMap* out, const uint8_t* x, int64_t M, int64_t K, int nt
     cache[key] = *out;
     return true;
 }
+}  // namespace
+
+// fireq_clear_cache: drop every cached TMA descriptor (they embed device pointers).
+void clear_x_map_cache() {
+    std::lock_guard<std::mutex> lock(x_map_mu());
+    x_map_cache().clear();
+}
+
+namespace {
 
 struct Plan {
     int ntok, m_tiles, n_tiles, tiles, G, mode, C, R, S;
@@ -1261,19 +1293,39 @@ fireq_status_t launch_cfg(const CUtensorMap& map, const GemmArgs& args, cudaStre
                           const CUtensorMap* map1 = nullptr, const GemmArgs* args1 = nullptr) {
     using C = Cfg<NTOK, SS, NCONV, STAGES, ASTAGES, ACCBUF, GPS, NMMA>;
     auto kern = k_w4a8_gemm<NTOK, SS, NCONV, STAGES, ASTAGES, ACCBUF, GPS, NMMA, NPH>;
-    static bool attr_done = false;
-    if (!attr_done) {
+    // the attribute is per device (a process may drive several GPUs)
+    static bool attr_done[kMaxDevices] = {};
+    static int resident[kMaxDevices] = {};     // CTAs of this kernel resident at once on the device
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
+        return fail(FIREQ_ERROR_CUDA, "cudaGetDevice failed");
+    if (!attr_done[dev]) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
             return fail(FIREQ_ERROR_CUDA, "cudaFuncSetAttribute(smem) failed");
-        attr_done = true;
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::kThreads, C::kSmemBytes) != cudaSuccess)
+            return fail(FIREQ_ERROR_CUDA, "cudaOccupancyMaxActiveBlocksPerMultiprocessor failed");
+        resident[dev] = per_sm * sm_count();
+        attr_done[dev] = true;
     }
     GemmArgs la = args;
     if (la.depth > STAGES - 2 || la.depth < 1) la.depth = STAGES;
     GemmArgs lb = args1 ? *args1 : la;
     if (lb.depth > STAGES - 2 || lb.depth < 1) lb.depth = STAGES;
     const CUtensorMap& m1 = map1 ? *map1 : map;
+    // CTAs that spin on other CTAs (stream-K owners, the fused FFN's grid barriers) need the
+    // whole grid resident, as CUTLASS's stream-K fixup does: the grid is at most one CTA per
+    // SM and is checked against the occupancy calculator.  Co-residency then holds unless
+    // another kernel holds SMs for the whole duration (concurrent streams, MPS / green
+    // contexts); FIREQ_COOPERATIVE=1 launches such grids cooperatively, which guarantees it
+    // (the launch fails instead of hanging) at ~1.4 us per launch (no PDL overlap, measured).
+    const bool spins = la.R > 0 || la.out_layout == 2 || (args1 && lb.R > 0);
+    if (spins && la.C > resident[dev])
+        return fail(FIREQ_ERROR_UNSUPPORTED_SHAPE, "fireq_w4a8_gemm: grid exceeds the resident CTAs of this device");
+    static const bool coop_env = getenv("FIREQ_COOPERATIVE") != nullptr;
+    const bool coop = spins && coop_env;
     const cudaError_t e = launch_ex(kern, dim3(la.C), dim3(C::kThreads), C::kSmemBytes, stream,
-                                    (unsigned)(la.S > 1 ? la.S : 1), map, la, m1, lb);
+                                    (unsigned)(la.S > 1 ? la.S : 1), coop, map, la, m1, lb);
     if (e != cudaSuccess) return fail(FIREQ_ERROR_CUDA, std::string("fireq_w4a8_gemm launch: ") + cudaGetErrorString(e));
     return check_launch("fireq_w4a8_gemm");
 }
@@ -1318,19 +1370,25 @@ GemmArgs base_args(const Plan& p, int64_t M, int64_t N, int64_t K, const uint8_t
     args.Cs = (unsigned)p.Cs;
     args.S = p.S;
     {
+#if FIREQ_PROFILE
         static const int depth = getenv("FIREQ_DEPTH") ? atoi(getenv("FIREQ_DEPTH")) : 1000;   // experiments
         args.depth = depth;
+#else
+        args.depth = 1000;
+#endif
     }
-    args.trace = g_trace;
+    args.trace = FIREQ_PROFILE ? g_trace : nullptr;
     args.pf_ptr[0] = static_cast<const uint8_t*>(pf0);
     args.pf_bytes[0] = pf0 ? (pf0_bytes & ~size_t(15)) : 0;
     args.pf_ptr[1] = static_cast<const uint8_t*>(pf1);
     args.pf_bytes[1] = pf1 ? (pf1_bytes & ~size_t(15)) : 0;
     args.span = next_span_slot();
-    {
+#if FIREQ_PROFILE
+    {   // experiments only (profile builds): skip parts of the work
         static const int dbg = getenv("FIREQ_DEBUG_MODE") ? atoi(getenv("FIREQ_DEBUG_MODE")) : 0;
         args.dbg = dbg;
     }
+#endif
     return args;
 }
 
@@ -1439,9 +1497,11 @@ fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_b
     a2.Y = y;
     a2.ldy = ldy;
     a2.out_layout = 0;
+#if FIREQ_PROFILE
     static const int trace_which = getenv("FIREQ_TRACE_WHICH") ? atoi(getenv("FIREQ_TRACE_WHICH")) : 0;  // debug
     if (trace_which == 2) a1.trace = nullptr;
     if (trace_which == 1) a2.trace = nullptr;
+#endif
     if (persistent && p1.C == p2.C)
         return launch_cfg<16, true, 3, 8, 3, 2, 2, 1, 2>(map1, a1, stream, &map2, &a2);
     st = launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map1, a1, stream);

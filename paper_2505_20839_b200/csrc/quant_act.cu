@@ -1,8 +1,10 @@
 // quant_act.cu -- fireq_quantize_act (A1..A3, Eq. 2, per token P:482) and the
 // FFN helper fireq_silu_mul_quantize_act (SiLU * up, then A2..A3).
 //
-// Each token row is split over a cluster of CL CTAs (CL = 8 at decode sizes); the
-// chunk is read twice (amax pass, encode pass; the second pass hits L1).
+// One CTA per token row: each thread keeps its 8-element vectors of x' in registers between
+// the amax pass and the encode pass (the kernel can also split a row over a cluster of CTAs
+// with a DSMEM amax reduction, but the launcher uses CL = 1: at decode sizes the cluster
+// launch and its two cluster barriers cost more latency than they save, measured).
 // Memory-bound: 2 B read + 1 B written per element.  Launched with PDL.
 #include <algorithm>
 
@@ -17,6 +19,9 @@ constexpr int kThreads = 256;
 // x / beta for the E4M3 encode: q0 = x * rcp(beta), one exact-residual correction (as the
 // SwiGLU tail of gemm.cu); see DESIGN reading R22 for why the E4M3 rounding is unchanged.
 __device__ __forceinline__ float q_div(float x, float beta, float rcp) {
+    // beta below the fp32 normal range: 1/beta may overflow (and its residual lose bits), so
+    // use the IEEE quotient (warp-uniform: one beta per row)
+    if (beta < 0x1p-126f) return __fdiv_rn(x, beta);
     const float q0 = __fmul_rn(x, rcp);
     const float e = __fmaf_rn(-q0, beta, x);
     // x = -0: the correction's +0 would lose the sign; OR-ing x's sign bit is a no-op otherwise
@@ -86,10 +91,9 @@ __device__ __forceinline__ uint4 xprime8(const Src& s, int64_t m, int64_t k) {
 }
 
 // Grid (CL, rows), cluster (CL, 1, 1): CTA `rank` of a cluster quantizes columns
-// [rank*K/CL, (rank+1)*K/CL) of token row m; the row amax is combined across the
-// cluster through distributed shared memory (DSMEM).  CL = 8 for decode-sized M
-// (spreads a 16-token batch over 128 CTAs), 1 for large M.  Each thread keeps its
-// (at most R) 8-element vectors of x' in registers between the amax and encode passes.
+// [rank*K/CL, (rank+1)*K/CL) of token row m; with CL > 1 the row amax is combined across
+// the cluster through distributed shared memory (DSMEM).  The launcher uses CL = 1.  Each
+// thread keeps its (at most R) 8-element vectors of x' in registers between the passes.
 template <int R>
 __global__ void __launch_bounds__(1024) k_act_quant(Src s, int64_t M, int64_t K, int cl,
                                                    uint8_t* __restrict__ xq,
@@ -163,7 +167,7 @@ template <int R>
 cudaError_t launch_act(const Src& s, int64_t M, int64_t K, int cl, int threads, uint8_t* xq, __nv_bfloat16* beta,
                        cudaStream_t stream) {
     const unsigned rows = (unsigned)std::min<int64_t>(M, 65535);
-    return launch_ex(k_act_quant<R>, dim3((unsigned)cl, rows), dim3(threads), 0, stream, (unsigned)cl, s, M, K, cl,
+    return launch_ex(k_act_quant<R>, dim3((unsigned)cl, rows), dim3(threads), 0, stream, (unsigned)cl, false, s, M, K, cl,
                      xq, beta, next_span_slot());
 }
 

@@ -24,7 +24,7 @@ EXPORTS = [
     "fireq_w4a8_gemm_colpar", "fireq_debug_lut_table", "fireq_gemm_plan", "fireq_debug_set_trace",
     "fireq_quantize_act_t", "fireq_silu_mul_quantize_act_t", "fireq_debug_set_spans",
     "fireq_w4a8_gemm_prefetch", "fireq_interleave_gate_up", "fireq_ffn_workspace_bytes",
-    "fireq_ffn_w4a8_decode",
+    "fireq_ffn_w4a8_decode", "fireq_clear_cache",
 ]
 
 
@@ -44,6 +44,7 @@ def load(path=LIB_PATH):
     sig = {
         "fireq_status_string": ([C], ctypes.c_char_p),
         "fireq_last_error": ([], ctypes.c_char_p),
+        "fireq_clear_cache": ([], None),
         "fireq_weight_layout_version": ([], C),
         "fireq_packed_weight_bytes": ([I64, I64], SZ),
         "fireq_weight_scale_bytes": ([I64, I64], SZ),
@@ -100,6 +101,21 @@ def _ptr(t):
 def _stream(stream=None):
     s = stream if stream is not None else torch.cuda.current_stream()
     return ctypes.c_void_p(s.cuda_stream)
+
+
+def _zeros_on(nbytes, device, stream=None):
+    """Zeroed uint8 scratch allocated AND zeroed on `stream` (the stream the kernel is
+    enqueued on): the memset is ordered before the kernel, and the caching allocator
+    frees it in that stream's order."""
+    if stream is None:
+        return torch.zeros(int(nbytes), dtype=torch.uint8, device=device)
+    with torch.cuda.stream(stream):
+        return torch.zeros(int(nbytes), dtype=torch.uint8, device=device)
+
+
+def clear_cache():
+    """fireq_clear_cache: drop the library's cached TMA descriptors."""
+    lib().fireq_clear_cache()
 
 
 # ------------------------------------------------------------------- sizes
@@ -227,12 +243,13 @@ def silu_mul_quantize_act_t(Gt, Ut, M, K, stream=None, out=None):
 class Workspace:
     """Zero-initialised GEMM workspace (the counters must start at zero, fireq.h)."""
 
-    def __init__(self, nbytes, device="cuda"):
-        self.t = torch.zeros(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+    def __init__(self, nbytes, device="cuda", stream=None):
+        self.t = _zeros_on(max(int(nbytes), 256), device, stream)
 
-    def ensure(self, nbytes):
+    def ensure(self, nbytes, stream=None):
+        """Grow (re-zeroed on `stream`, the stream of the kernel that will use it)."""
         if self.t.numel() < nbytes:
-            self.t = torch.zeros(int(nbytes), dtype=torch.uint8, device=self.t.device)
+            self.t = _zeros_on(nbytes, self.t.device, stream)
         return self.t
 
 
@@ -246,7 +263,7 @@ def w4a8_gemm(xq, beta, packed, scales, N, pts_n, gamma=None, out=None, out_layo
     M, K = xq.shape
     L = lib()
     need = L.fireq_w4a8_gemm_workspace_bytes(M, N, K)
-    ws = workspace.ensure(need) if workspace is not None else torch.zeros(need, dtype=torch.uint8, device=xq.device)
+    ws = workspace.ensure(need, stream) if workspace is not None else _zeros_on(need, xq.device, stream)
     if out is None:
         out = torch.empty((M, N) if out_layout == 0 else (N, M), dtype=torch.bfloat16, device=xq.device)
     ldy = out.stride(0)
@@ -287,7 +304,7 @@ def ffn_w4a8_decode(x, q_gu, q_d, h=None, out=None, workspace=None, stream=None,
     d_ff = q_d.K
     L = lib()
     need = L.fireq_ffn_workspace_bytes(M, d_model, d_ff)
-    ws = workspace.ensure(need) if workspace is not None else torch.zeros(need, dtype=torch.uint8, device=x.device)
+    ws = workspace.ensure(need, stream) if workspace is not None else _zeros_on(need, x.device, stream)
     if h is None:
         h = torch.empty((M, d_ff), dtype=torch.bfloat16, device=x.device)
     if out is None:
@@ -346,7 +363,7 @@ def w4a8_gemm_colpar(xq, beta, packed_local, scales_local, N_local, pts_n, comm,
                      gamma_local=None, stream=None):
     """Column-parallel GEMM: this rank's Y^T slice + in-place NCCL all-gather into Yt_full [P*N_local][M]."""
     M, K = xq.shape
-    ws = workspace.ensure(lib().fireq_w4a8_gemm_workspace_bytes(M, N_local, K))
+    ws = workspace.ensure(lib().fireq_w4a8_gemm_workspace_bytes(M, N_local, K), stream)
     _check(lib().fireq_w4a8_gemm_colpar(_ptr(xq), _ptr(beta), M, K, _ptr(packed_local), _ptr(scales_local), N_local,
                                         pts_n, _ptr(gamma_local), _ptr(Yt_full), _ptr(ws), ws.numel(), comm.h,
                                         _stream(stream)),

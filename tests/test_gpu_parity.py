@@ -131,7 +131,10 @@ def test_quantize_act_exhaustive_bf16(fireq):
     must give the oracle's E4M3 codes bit-exactly (DESIGN reading R22)."""
     pos = np.arange(0x0000, 0x7F80, dtype=np.uint32)            # all finite non-negative bf16 patterns
     vals = (pos << 16).astype(np.uint32).view(np.float32).astype(np.float64)
-    amaxes = [448.0, 1.0, 3.140625, 0.0078125 * 1.5, 2.0 ** -100 * 1.75, 57344.0, 1.0e30]
+    # ... plus rows whose beta = bf16(amax / 448) is below the fp32 normal range (1/beta
+    # overflows: the encoder must fall back to the IEEE quotient)
+    amaxes = [448.0, 1.0, 3.140625, 0.0078125 * 1.5, 2.0 ** -100 * 1.75, 57344.0, 1.0e30,
+              2.0 ** -120, 2.0 ** -125 * 1.5]
     rows = []
     for A in amaxes:
         A = float(nm.bf16_rn(np.array([A]))[0])
@@ -222,10 +225,26 @@ def test_gemm_hybrid_few_remainder_units(fireq, M, N, K):
     assert og.rel_frobenius(y, r) < 5e-3
 
 
-@pytest.mark.parametrize("M", [16, 200])
+@pytest.mark.parametrize("M", [16, 200, 13, 2100])
 def test_gemm_transposed_output_and_gamma(fireq, M):
+    """Y^T (the column-parallel layout) with gamma; M = 13: ldy = 13 (no 16-B row stores);
+    M = 2100: ten 224-token m-tiles, consecutive segments of a CTA in different m-tiles (the
+    per-token scales of one segment must not be overwritten by a warp already in the next)."""
     y, r, *_ = run_case(fireq, M, 256, 512, gamma=True, out_layout=1, seed=M)
     assert og.g4_error(y, r) <= G4_TOL
+
+
+def test_gemm_transposed_many_mtiles_equals_row_major(fireq):
+    """Y^T and Y of the same GEMM (same plan) agree bit for bit at many m-tiles per CTA."""
+    M, N, K = 4100, 384, 256
+    wb = synth.weights(N, K, 901)
+    xb = synth.activations(M, K, 902)
+    qw = fireq.quantize_weight(to_dev_bf16(wb))
+    xq, beta = fireq.quantize_act(to_dev_bf16(xb), chan_mul=qw.c)
+    g = torch.rand(N, device=DEV) + 0.5
+    y = fireq.w4a8_gemm(xq, beta, qw.packed, qw.scales, N, qw.n, gamma=g)
+    yt = fireq.w4a8_gemm(xq, beta, qw.packed, qw.scales, N, qw.n, gamma=g, out_layout=1)
+    assert torch.equal(y, yt.t())
 
 
 def test_gemm_exactness_corridor(fireq):
@@ -304,3 +323,117 @@ def test_gemm_full_size_sampled(fireq, name, M):
     r = og.reference_rows(rq, rbeta, wdeq, ref.n)
     y = Y.float().cpu().numpy().astype(np.float64)[:, rows]
     assert og.g4_error(y, r) <= G4_TOL
+
+
+def _sampled_parity(fireq, wb, Ms, gamma=False, n_chan=160, n_tok=48, seed=0):
+    """Full-size GEMM in the bench's launch configuration vs the oracle on sampled outputs.
+
+    The GPU quantizes the whole weight; the oracle computes CAS lambda and the PTS exponent
+    over the whole tensor (global) and W4-W5 for the sampled channels only (per-row
+    steps).  For each M in Ms the GPU runs the whole GEMM; the oracle forms the fp64 reference
+    for n_tok sampled tokens x n_chan sampled channels (activation rows are quantized
+    independently, A1-A3), and the GPU's X_hat / beta of the sampled tokens must equal the
+    oracle's bit for bit.
+    """
+    N, K = wb.shape
+    rng = np.random.default_rng(seed)
+    chans = np.sort(rng.choice(N, n_chan, replace=False))
+    qw = fireq.quantize_weight(to_dev_bf16(wb), cas_mode=1)
+    torch.cuda.synchronize()
+    ref = oq.quantize_weight(synth.bits_to_f64(wb), 1, pack=False, rows=chans)
+    assert qw.n == ref.n
+    assert np.array_equal(bits_of(qw.c), nm.bf16_to_bits(ref.c))
+    # GPU packing of some sampled rows == oracle codes / scale codes
+    packed = qw.packed.cpu().numpy()
+    scales = qw.scales.cpu().numpy()
+    kk = np.arange(K)
+    for i in range(0, n_chan, n_chan // 8):
+        n = chans[i]
+        byte, half = ol.packed_byte_index(np.full(K, n), kk, K)
+        nib = np.where(half == 0, packed[byte] & 15, packed[byte] >> 4).astype(np.int16)
+        assert np.array_equal(np.where(nib >= 8, nib - 16, nib), ref.codes[i])
+        assert np.array_equal(scales[ol.scale_index(np.full(K // 128, n), np.arange(K // 128), K)],
+                              ref.sigma_codes[i])
+    del packed
+    table = og.lut_of_luts()
+    wdeq = nm.E4M3_DECODE[table[np.repeat(ref.sigma_codes.astype(np.int64), 128, axis=1),
+                                ref.codes.astype(np.int64) & 15]]
+    g_np = gam = None
+    if gamma:
+        g_np = nm.f32(rng.uniform(0.5, 2.0, N))
+        gam = torch.from_numpy(g_np.astype(np.float32)).to(DEV)
+    errs = {}
+    for M in Ms:
+        xb = synth.activations(M, K, synth.layer_seed(5, M))
+        xd = to_dev_bf16(xb)
+        xq, beta = fireq.quantize_act(xd, chan_mul=qw.c)
+        del xd
+        Y = fireq.w4a8_gemm(xq, beta, qw.packed, qw.scales, N, qw.n, gamma=gam)
+        torch.cuda.synchronize()
+        toks = np.arange(M) if M <= n_tok else np.sort(np.concatenate(
+            [[0, M - 1], rng.choice(np.arange(1, M - 1), n_tok - 2, replace=False)]))
+        tk = torch.from_numpy(toks).to(DEV)
+        rq, rbeta = oq.quantize_act(synth.bits_to_f64(xb[toks]), ref.c)
+        assert np.array_equal(xq[tk].cpu().numpy(), rq)
+        assert np.array_equal(bits_of(beta[tk]), nm.bf16_to_bits(rbeta))
+        r = og.reference_rows(rq, rbeta, wdeq, ref.n, gamma_rows=None if g_np is None else g_np[chans])
+        y = Y[tk][:, torch.from_numpy(chans).to(DEV)].float().cpu().numpy().astype(np.float64)
+        errs[M] = og.g4_error(y, r)
+        del Y, xq, beta
+        torch.cuda.empty_cache()
+    assert all(e <= G4_TOL for e in errs.values()), errs
+    return errs
+
+
+def test_gemm_bench_gate_up_full_size(fireq):
+    """The headline bench GEMM exactly: Llama2-7B [gate; up] 22016 x 4096 quantized as ONE
+    matrix (reading R20), with a per-channel gamma, at M = 16 (hybrid whole-tile + stream-K
+    plan) and at the prefill size M = 16 x 1024."""
+    wg = synth.weights(11008, 4096, synth.layer_seed(1, 0))
+    wu = synth.weights(11008, 4096, synth.layer_seed(1, 1))
+    plan = fireq.gemm_plan(16, 22016, 4096)
+    assert plan["mode"] == "stream-k" and plan["ctas"] == 148, plan
+    _sampled_parity(fireq, np.concatenate([wg, wu], axis=0), [16, 16384], gamma=True)
+
+
+@pytest.mark.parametrize("name", ["llama2-70b.gate", "llama2-70b.down", "llama3-8b.down"])
+def test_gemm_large_shapes_sampled(fireq, name):
+    """BASELINE C4 (Llama2-70B FFN, K up to 28672 -- the longest accumulation) and C3/C5's
+    Llama3-8B down_proj, at decode M = 16 and prefill M = 16384."""
+    N, K = synth.SHAPES[name]
+    _sampled_parity(fireq, synth.weights(N, K, synth.layer_seed(4, N + K)), [16, 16384])
+
+
+def test_cooperative_launch_same_result(fireq):
+    """FIREQ_COOPERATIVE=1 (co-residency guaranteed by a cooperative launch, also inside a
+    CUDA graph) gives the same bits as the default launch for a stream-K plan."""
+    import os, subprocess, sys
+    M, N, K = 16, 22016, 1024
+    wb = synth.weights(N, K, 1501)
+    xb = synth.activations(M, K, 1502)
+    qw = fireq.quantize_weight(to_dev_bf16(wb))
+    xq, beta = fireq.quantize_act(to_dev_bf16(xb), chan_mul=qw.c)
+    y = fireq.w4a8_gemm(xq, beta, qw.packed, qw.scales, N, qw.n).cpu()
+    assert fireq.gemm_plan(M, N, K)["mode"] == "stream-k"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, torch; sys.path.insert(0, %r)\n"
+        "import synth\n"
+        "from paper_2505_20839_b200 import fireq as F; F.load()\n"
+        "wb = synth.weights(%d, %d, 1501); xb = synth.activations(%d, %d, 1502)\n"
+        "qw = F.quantize_weight(synth.bits_to_torch(wb).cuda())\n"
+        "xq, beta = F.quantize_act(synth.bits_to_torch(xb).cuda(), chan_mul=qw.c)\n"
+        "ws = F.Workspace(F.gemm_workspace_bytes(%d, %d, %d)); out = torch.empty(%d, %d, dtype=torch.bfloat16, device='cuda')\n"
+        "s = torch.cuda.Stream()\n"
+        "F.w4a8_gemm(xq, beta, qw.packed, qw.scales, %d, qw.n, out=out, workspace=ws, stream=s); torch.cuda.synchronize()\n"
+        "g = torch.cuda.CUDAGraph()\n"
+        "with torch.cuda.graph(g, stream=s):\n"
+        "    F.w4a8_gemm(xq, beta, qw.packed, qw.scales, %d, qw.n, out=out, workspace=ws, stream=s)\n"
+        "out.zero_(); g.replay(); torch.cuda.synchronize()\n"
+        "torch.save(out.cpu(), sys.argv[1])\n") % (root, N, K, M, K, M, N, K, M, N, N, N)
+    tmp = os.path.join(root, "gpurun_out", "coop_y.pt")
+    os.makedirs(os.path.dirname(tmp), exist_ok=True)
+    r = subprocess.run([sys.executable, "-c", code, tmp], env=dict(os.environ, FIREQ_COOPERATIVE="1"),
+                       capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert torch.equal(torch.load(tmp), y)

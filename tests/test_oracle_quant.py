@@ -12,6 +12,8 @@ import numpy as np
 import pytest
 
 from oracle import gemm, layout, quant
+from oracle import quant as oq
+import synth
 from oracle import numerics as nm
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
@@ -422,3 +424,20 @@ def test_underflow_group_fraction():
     assert quant.underflow_group_fraction(W) == 0.25
     n, _ = quant.pts_exponent(W)
     assert quant.underflow_group_fraction(W * 2.0 ** n) <= 0.25
+
+
+def test_quantize_weight_rows_subset_equals_full():
+    """rows= (used by the full-size GPU checks) computes W4-W5 of the selected rows only; CAS
+    and PTS stay global, so the subset must equal the same rows of the full computation."""
+    wb = synth.weights(512, 1024, 5)
+    W = synth.bits_to_f64(wb)
+    W[7, :] *= 0.0                       # rows that change nothing globally still select correctly
+    full = oq.quantize_weight(W, 1, pack=False)
+    rows = np.array([0, 7, 100, 511])
+    sub = oq.quantize_weight(W, 1, pack=False, rows=rows)
+    assert full.n == sub.n
+    assert np.array_equal(full.lam, sub.lam)
+    assert np.array_equal(full.codes[rows], sub.codes)
+    assert np.array_equal(full.sigma_codes[rows], sub.sigma_codes)
+    with pytest.raises(ValueError):
+        oq.quantize_weight(W, 1, rows=rows)
