@@ -275,66 +275,135 @@ def time_graphs(graphs, steps, warmup, stream, barrier=None):
 
 
 # ------------------------------------------------------------------ CPU oracle
-def cpu_oracle_sample(frac_rows=8, M=M_DECODE):
-    """The oracle (as it stands) on a bounded sample of the decode FFN step.
+def host_info():
+    """nproc, sockets and CPU model of the host the oracle runs on (lscpu)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                info[k.strip()] = v.strip()
+    except Exception:
+        pass
+    return info
 
-    Sample: the activation quantizer on the full token batch, and the three fp64
-    reference GEMMs (LUT dequantization + matmul) on 1/frac_rows of the output
-    channels with full K; the time is scaled by frac_rows to one FFN step.
-    Weight quantization (offline) is not part of the step, as on the GPU side.
-    """
-    from oracle import gemm as og, quant as oq, ffn as of, numerics as nm
+
+def blas_threads():
     try:
         from threadpoolctl import threadpool_info
-        threads = max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
+        return max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
     except Exception:
-        threads = 1
-    rng = np.random.default_rng(0)
-    X = synth.bits_to_f64(synth.activations(M, D_MODEL, 1))
-    H = synth.bits_to_f64(synth.activations(M, D_FF, 2))
-    ng, nd = D_FF * 2 // frac_rows // 128 * 128, D_MODEL // frac_rows // 128 * 128
-    codes_gu = rng.integers(-8, 8, (ng, D_MODEL)).astype(np.int8)
-    codes_d = rng.integers(-8, 8, (nd, D_FF)).astype(np.int8)
-    from oracle import layout as ol
-    p_gu = ol.pack_codes(codes_gu)
-    s_gu = ol.pack_scales(rng.integers(40, 60, (ng, D_MODEL // 128)).astype(np.uint8))
-    p_d = ol.pack_codes(codes_d)
-    s_d = ol.pack_scales(rng.integers(40, 60, (nd, D_FF // 128)).astype(np.uint8))
-    c = nm.bf16_rn(np.ones(D_MODEL))
-    t0 = time.perf_counter()
-    xq, beta = oq.quantize_act(X, c)
-    r = og.gemm_reference(xq, beta, p_gu, s_gu, ng, D_MODEL, 10)
-    h = of.silu_mul(nm.bf16_rn(r[:, : ng // 2]), nm.bf16_rn(r[:, ng // 2:]))
-    hq, hb = oq.quantize_act(H)
-    og.gemm_reference(hq, hb, p_d, s_d, nd, D_FF, 10)
-    dt = time.perf_counter() - t0
-    # act quant of h on the full width is included; GEMM parts scale with the sampled rows
-    est = dt * frac_rows
-    return {"value": est * 1e6, "unit": "us", "cores": threads, "kind": "oracle",
-            "sample": f"activation quantizer on the full [16][4096] batch + fp64 LUT-dequant reference GEMMs on "
-                      f"1/{frac_rows} of the output channels of gate_up ({ng} rows) and down ({nd} rows), full K; "
-                      f"time x{frac_rows} = one FFN step; measured {dt:.2f} s"}
+        return 1
+
+
+class OracleFFN:
+    """The oracle's Llama2-7B FFN step (decode batch 16), as it stands: A1-A3 on x, the
+    fp64 LUT-dequant reference GEMM over the full [gate; up] (22016 x 4096), SiLU * up,
+    A2-A3 on h, the fp64 reference down GEMM (4096 x 11008).  Weights are packed codes
+    and scale codes (layout v1) drawn at random: the oracle's time does not depend on
+    their values; the GPU arm's weights are quantized offline the same way."""
+
+    def __init__(self, M=M_DECODE):
+        from oracle import numerics as nm
+        rng = np.random.default_rng(0)
+        self.M = M
+        self.X = synth.bits_to_f64(synth.activations(M, D_MODEL, 1))
+        self.c = nm.bf16_rn(np.exp(rng.normal(0.0, 0.3, D_MODEL)))
+        self.p_gu = rng.integers(0, 256, 2 * D_FF * D_MODEL // 2, dtype=np.uint8)
+        self.s_gu = rng.integers(40, 60, 2 * D_FF * D_MODEL // 128).astype(np.uint8)
+        self.p_d = rng.integers(0, 256, D_MODEL * D_FF // 2, dtype=np.uint8)
+        self.s_d = rng.integers(40, 60, D_MODEL * D_FF // 128).astype(np.uint8)
+
+    def step(self):
+        """One full FFN step; returns {phase: seconds} (no sampling, no extrapolation)."""
+        from oracle import gemm as og, quant as oq, ffn as of, numerics as nm
+        t0 = time.perf_counter()
+        xq, beta = oq.quantize_act(self.X, self.c)
+        t1 = time.perf_counter()
+        r = og.gemm_reference(xq, beta, self.p_gu, self.s_gu, 2 * D_FF, D_MODEL, 10)
+        t2 = time.perf_counter()
+        h = of.silu_mul(nm.bf16_rn(r[:, :D_FF]), nm.bf16_rn(r[:, D_FF:]))
+        hq, hb = oq.quantize_act(h)
+        t3 = time.perf_counter()
+        og.gemm_reference(hq, hb, self.p_d, self.s_d, D_MODEL, D_FF, 10)
+        t4 = time.perf_counter()
+        return {"quantize_act_x": t1 - t0, "gemm_gate_up": t2 - t1, "silu_mul_quantize_act_h": t3 - t2,
+                "gemm_down": t4 - t3, "total": t4 - t0}
+
+
+def oracle_c1_phases(reps=3):
+    """BASELINE configs[0] (C1: q_proj 4096 x 4096, M = 16) per phase: quantize-weight,
+    quantize-act, fp64 reference GEMM -- median of `reps` with all BLAS threads, and one run
+    with a single thread."""
+    from oracle import gemm as og, quant as oq
+    W = synth.bits_to_f64(synth.weights(4096, 4096, synth.layer_seed(0, 0)))
+    X = synth.bits_to_f64(synth.activations(16, 4096, synth.layer_seed(0, 1)))
+
+    def once():
+        t0 = time.perf_counter()
+        q = oq.quantize_weight(W, 1)
+        t1 = time.perf_counter()
+        xq, beta = oq.quantize_act(X, q.c)
+        t2 = time.perf_counter()
+        og.gemm_reference(xq, beta, q.packed, q.scales, 4096, 4096, q.n)
+        t3 = time.perf_counter()
+        return t1 - t0, t2 - t1, t3 - t2
+
+    runs = [once() for _ in range(reps)]
+    med = [statistics.median(r[i] for r in runs) for i in range(3)]
+    one = None
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1):
+            one = once()
+    except Exception:
+        pass
+    ms = lambda v: round(v * 1e3, 2)
+    out = {"workload": "C1 q_proj M=16 K=4096 N=4096", "threads": blas_threads(),
+           "quantize_weight_ms": ms(med[0]), "quantize_act_ms": ms(med[1]), "gemm_ms": ms(med[2])}
+    if one:
+        out["one_thread"] = {"quantize_weight_ms": ms(one[0]), "quantize_act_ms": ms(one[1]), "gemm_ms": ms(one[2])}
+    return out
+
+
+def cpu_oracle_baseline():
+    """cpu_baseline of the GPU arm: one FULL oracle FFN step (the metric's unit, no scaling)
+    with its phases, plus C1's per-phase times, on this host's cores."""
+    ffn = OracleFFN()
+    ph = ffn.step()
+    return {"value": round(ph["total"] * 1e6, 1), "unit": "us", "cores": blas_threads(), "kind": "oracle",
+            "sample": "one full Llama2-7B FFN step at batch 16 (act-quant x, fp64 LUT-dequant gate_up 22016x4096, "
+                      "SiLU*up + act-quant h, fp64 down 4096x11008); no sampling or extrapolation",
+            "phases_ms": {k: round(v * 1e3, 1) for k, v in ph.items() if k != "total"},
+            "c1": oracle_c1_phases(), "host": host_info()}
 
 
 # ------------------------------------------------------------------ arms
 def run_reference(args, rank, world):
+    """--impl reference: there is no installable reference implementation (the reference is a
+    paper), so this arm times the CPU oracle as it stands: every step is one FULL oracle FFN
+    step (about 8 s on a 16-core host), so value x steps is the wall time of the timed loop."""
     if rank != 0:
         return
-    vals = []
-    for _ in range(max(1, args.warmup)):
-        cpu_oracle_sample(frac_rows=32)
-    samples = []
-    for _ in range(args.steps):
-        samples.append(cpu_oracle_sample(frac_rows=32))
-    v = statistics.median([s["value"] for s in samples])
-    cb = dict(samples[0])
-    cb["value"] = v
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "us", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v / 1e3, "higher_is_better": False,
+    ffn = OracleFFN()
+    for _ in range(args.warmup):
+        ffn.step()
+    t0 = time.perf_counter()
+    steps = [ffn.step() for _ in range(args.steps)]
+    wall = time.perf_counter() - t0
+    v = statistics.median(s["total"] for s in steps) * 1e6
+    cb = {"value": round(v, 1), "unit": "us", "cores": blas_threads(), "kind": "oracle",
+          "sample": f"{args.steps} full Llama2-7B FFN steps at batch 16 (median), no extrapolation; timed loop "
+                    f"{wall:.1f} s", "host": host_info(),
+          "phases_ms": {k: round(statistics.median(s[k] for s in steps) * 1e3, 1) for k in steps[0] if k != "total"}}
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 1), "unit": "us", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v / 1e3, 3), "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "llama2-7b-ffn-decode-b16", "tokens": M_DECODE, "d_model": D_MODEL,
                        "d_ff": D_FF},
-            "cpu_baseline": cb, "e2e": {"value": v, "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": cb, "e2e": {"value": round(v, 1), "unit": "us", "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -432,7 +501,7 @@ def run_fireq(args, rank, world, dev):
     pre_info = prefill_figures(F, dev, stream, peaks) if not args.no_prefill else None
 
     # ---------------- cpu baseline (oracle on a bounded sample)
-    cpu = cpu_oracle_sample(frac_rows=8) if not args.no_cpu else None
+    cpu = cpu_oracle_baseline() if not args.no_cpu else None
 
     hbm = peaks["hbm_gbs"]
     line = {
@@ -451,7 +520,9 @@ def run_fireq(args, rank, world, dev):
         "fused_ffn_api_us": round(fused_us, 3),
         "roofline": {"bound": "hbm", "kernel": "fireq_w4a8_gemm gate_up M=16 N=22016 K=4096",
                      "achieved": round(gbs_gu, 1), "peak": hbm, "unit": "GB/s", "frac": round(gbs_gu / hbm, 4),
-                     "traffic": traffic, "algorithmic_bytes": b_gu, "launch_us": round(ms_gu * 1e3, 3),
+                     "traffic": traffic, "traffic_source": "stored: profiles/traffic.json, ncu --set full "
+                     "dram__bytes_read.sum + dram__bytes_write.sum of this kernel (not measured in this run)",
+                     "algorithmic_bytes": b_gu, "launch_us": round(ms_gu * 1e3, 3),
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"},
         "gemm_down": {"us": round(ms_d * 1e3, 3), "gbs": round(gbs_d, 1), "frac": round(gbs_d / hbm, 4)},
         "e2e": {"value": round(e2e_ms * 1e3, 3), "unit": "us", "h2d_bytes_per_step": ffn.x.numel() * 2,
