@@ -212,8 +212,9 @@ class FusedFFN:
     def step(self, r, stream=None):
         q_gu, q_d = self.rot[r]
         nxt = self.rot[(r + 1) % len(self.rot)][0]
+        pf = (nxt.packed, nxt.scales) if os.environ.get("BENCH_PREFETCH", "1") == "1" else None
         self.F.ffn_w4a8_decode(self.x, q_gu, q_d, h=self.h, out=self.y, workspace=self.ws, stream=stream,
-                               prefetch=(nxt.packed, nxt.scales))
+                               prefetch=pf)
 
     def bytes_per_step(self):
         M = self.M

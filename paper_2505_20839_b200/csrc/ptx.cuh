@@ -39,6 +39,18 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
         : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
     return ok != 0;
 }
+// Polling wait (no HW suspend): test_wait + nanosleep back-off.
+__device__ __forceinline__ void mbar_wait_poll(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "POLL_%=:\n\t"
+        "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "nanosleep.u32 20;\n\t"
+        "bra POLL_%=;\n\t"
+        "DONE_%=:\n\t}"
+        ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
 // Non-blocking probe of a phase (no suspend): lets a warp overlap the round trip of the
 // NEXT stage's barrier with the current stage's work.
 __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
@@ -50,8 +62,21 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
         : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
     return ok != 0;
 }
+// Blocking wait with the retry loop INSIDE the asm: the compiler sees straight-line code,
+// so warp-uniform values computed around the wait stay in uniform registers (a C++ retry
+// loop has a per-thread exit condition; after it, the MMA issuer re-derived its operands
+// with R2UR moves, ~10 per group at ~20+ cycles each, measured).
+// The suspend-time hint (ns) keeps a waiting warp asleep until the phase completes (it is
+// woken by the completion): without it try_wait returns after a short system limit and the
+// retry loop takes issue slots from the warps sharing its SM sub-partition -- the MMA warp
+// spinning on SMSP 3 slowed the converter warps there by ~40% (measured per warp).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    while (!mbar_try_wait(bar, parity)) { }
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}"
+        ::"r"(smem_u32(bar)), "r"(parity), "r"(0x100000u) : "memory");
 }
 
 // ------------------------------------------------------------------ TMA
@@ -63,6 +88,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32
         " [%0], [%1], %2, [%3], %4;"
         ::"r"(smem_u32(dst_smem)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
+}
+// 16-byte asynchronous global -> shared copy (LDGSTS; L2 only), zero-filled when src_bytes = 0.
+__device__ __forceinline__ void cp_async_16(void* dst_smem, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+                 ::"r"(smem_u32(dst_smem)), "l"(src), "r"(src_bytes) : "memory");
+}
+// Arrive on bar when all of this thread's prior cp.async copies have completed (the arrival is
+// counted against the barrier's expected count: .noinc).
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Generic-proxy shared-memory writes -> async-proxy (tensor core) reads.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 // 2-D tiled tensor copy global -> shared (coordinates innermost first).
 __device__ __forceinline__ void tma_2d_g2s(void* dst_smem, const CUtensorMap* map, int c0, int c1,
