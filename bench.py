@@ -500,6 +500,9 @@ def run_fireq(args, rank, world, dev):
     chain_info = decode_chain_figures(F, dev, stream, peaks)
     chain_info["fused_qkv_gate_up"] = decode_chain_figures(F, dev, stream, peaks, fused=True)
     pre_info = prefill_figures(F, dev, stream, peaks) if not args.no_prefill else None
+    # BASELINE configs[3] at P = 1 (the column-parallel runs report P = 2/4/8)
+    from paper_2505_20839_b200.c4 import c4_figures
+    c4_info = c4_figures(F, dev, stream, 0, 1, comm=None) if not args.no_c4 else None
 
     # ---------------- cpu baseline (oracle on a bounded sample)
     cpu = cpu_oracle_baseline() if not args.no_cpu else None
@@ -534,6 +537,8 @@ def run_fireq(args, rank, world, dev):
     line["decode_chain"] = chain_info
     if pre_info:
         line["prefill"] = pre_info
+    if c4_info:
+        line["c4_llama2_70b_ffn"] = c4_info
     if cpu:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
@@ -646,6 +651,7 @@ def main():
     ap.add_argument("--impl", choices=["fireq", "reference"], default="fireq")
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the Llama2-70B column-parallel figures")
     ap.add_argument("--colpar", action="store_true", help="column-parallel path even at N=1 (testing)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -660,6 +666,9 @@ def main():
     dev = torch.device("cuda", local)
     dist_on = world > 1 or args.colpar
     if dist_on:
+        # NCCL may print its version on stdout; the bench's stdout is ONE JSON line
+        if not os.environ.get("FIREQ_KEEP_NCCL_DEBUG"):
+            os.environ["NCCL_DEBUG"] = "WARN"
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         os.environ.setdefault("RANK", str(rank))

@@ -1184,7 +1184,11 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, bool allow_cluster = true) {
     p.tiles = p.m_tiles * p.n_tiles;
     p.G = (int)(K / kGroup);
     const int sms = sm_count();
-    if (p.tiles >= 2 * sms) {
+    // decode tiles (NTOK <= 32) whose count is not a multiple of the SM count split the last
+    // partial wave stream-K as well: whole-tile round robin would leave e.g. 4 of 448 tiles
+    // (Llama2-70B gate_up, M = 16) for a 4th wave that 144 SMs sit out (~25% of the launch)
+    const bool split_tail = p.ntok <= 32 && p.tiles % sms != 0;
+    if (p.tiles >= 2 * sms && !split_tail) {
         // many tiles: whole tiles round-robin (last-wave imbalance < 1/2 of a tile per CTA)
         p.R = 0;
         p.C = sms;

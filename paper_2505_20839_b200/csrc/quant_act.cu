@@ -171,15 +171,87 @@ cudaError_t launch_act(const Src& s, int64_t M, int64_t K, int cl, int threads, 
                      xq, beta, next_span_slot());
 }
 
+// ---------------------------------------------------------------------------------------
+// Transposed inputs at large M (the column-parallel path's Y^T, element (m, k) at X[k * ld + m]):
+// one CTA per block of 32 tokens (256 threads: warp w reads rows k = w, w + 8, ..., 64 contiguous
+// bytes each; 128-token CTAs measured 3x slower -- too few CTAs in flight).  Pass 1:
+// per-token max |x'| (A2); pass 2 re-reads, encodes (A3) into a shared [128 tokens][64 k] tile
+// and writes each token's 64 codes as 16-byte stores.  x' (A1 / SiLU*mul) is formed exactly as
+// in k_act_quant.
+constexpr int kTT = 32;        // tokens per CTA
+constexpr int kTK = 64;        // rows per pass-2 chunk
+constexpr int kTRow = 8;       // row interleave (256 threads = 32 tokens x 8 rows)
+__device__ __forceinline__ float xprime_t(const Src& s, int64_t m, int64_t k) {
+    const float x = __bfloat162float(s.X[k * s.ld + m]);
+    if (s.mode == 0) return x;
+    if (s.mode == 1) return __bfloat162float(__float2bfloat16_rn(__fmul_rn(x, __bfloat162float(s.c[k]))));
+    const float u = __bfloat162float(s.U[k * s.ld + m]);
+    const float silu = __fdividef(x, 1.0f + __expf(-x));
+    return __bfloat162float(__float2bfloat16_rn(__fmul_rn(silu, u)));
+}
+
+__global__ void __launch_bounds__(256) k_act_quant_t(Src s, int64_t M, int64_t K, uint8_t* __restrict__ xq,
+                                                     __nv_bfloat16* __restrict__ beta_out) {
+    __shared__ float red[kTRow][kTT];
+    __shared__ float sb[2][kTT];
+    __shared__ __align__(16) uint8_t tile[kTT][kTK];
+    ptx::pdl_trigger();
+    ptx::pdl_wait();
+    const int tl = threadIdx.x & (kTT - 1), kr = threadIdx.x / kTT;     // token in block, row phase
+    const int64_t m = (int64_t)blockIdx.x * kTT + tl;
+    const bool valid = m < M;
+    float amax = 0.0f;
+    if (valid)
+        for (int64_t k = kr; k < K; k += kTRow) amax = fmaxf(amax, fabsf(xprime_t(s, m, k)));
+    red[kr][tl] = amax;
+    __syncthreads();
+    if (kr == 0) {
+        float v = red[0][tl];
+#pragma unroll
+        for (int q = 1; q < kTRow; ++q) v = fmaxf(v, red[q][tl]);
+        const __nv_bfloat16 bh = v > 0.0f ? __float2bfloat16_rn(__fdiv_rn(v, 448.0f)) : __float2bfloat16_rn(1.0f);
+        sb[0][tl] = __bfloat162float(bh);
+        sb[1][tl] = __frcp_rn(__bfloat162float(bh));
+        if (valid) beta_out[m] = bh;
+    }
+    __syncthreads();
+    const float beta = sb[0][tl], rcp = sb[1][tl];
+    for (int64_t k0 = 0; k0 < K; k0 += kTK) {
+#pragma unroll 4
+        for (int kk = kr; kk < kTK; kk += kTRow) {
+            const float v = valid ? q_div(xprime_t(s, m, k0 + kk), beta, rcp) : 0.0f;
+            tile[tl][kk] = (uint8_t)(e4m3x2_rn(v, 0.0f) & 0xFFu);
+        }
+        __syncthreads();
+        // 32 tokens x 64 codes = 128 16-byte pieces
+        if (threadIdx.x < kTT * kTK / 16) {
+            const int t = threadIdx.x >> 2, piece = threadIdx.x & 3;
+            const int64_t mt = (int64_t)blockIdx.x * kTT + t;
+            if (mt < M)
+                *reinterpret_cast<uint4*>(xq + mt * K + k0 + piece * 16) =
+                    *reinterpret_cast<const uint4*>(&tile[t][piece * 16]);
+        }
+        __syncthreads();
+    }
+}
+
 }  // namespace
 
 fireq_status_t quantize_act_impl(const __nv_bfloat16* X, const __nv_bfloat16* U, int64_t M, int64_t K,
                                  int64_t ld, const __nv_bfloat16* c, int mode, bool transposed, uint8_t* xq,
                                  __nv_bfloat16* beta, cudaStream_t stream) {
     Src s{X, U, c, mode, transposed ? 1 : 0, ld};
+    if (transposed && M >= 64) {
+        const cudaError_t e = launch_ex(k_act_quant_t, dim3((unsigned)((M + kTT - 1) / kTT)), dim3(256), 0, stream, 1u,
+                                        false, s, M, K, xq, beta);
+        if (e != cudaSuccess) return fail(FIREQ_ERROR_CUDA, std::string("act quant launch: ") + cudaGetErrorString(e));
+        return check_launch(mode == 2 ? "fireq_silu_mul_quantize_act_t" : "fireq_quantize_act_t");
+    }
     // One CTA per token row (a cluster/DSMEM split of the row measured slower at decode:
     // cluster launch + two cluster barriers cost more latency than they save).
-    const int cl = 1;
+    // (transposed decode inputs read 2-byte elements at a stride of M: split each row over a
+    // cluster of 8 CTAs so that 8x more loads are in flight)
+    const int cl = (transposed && (K / 8) % 8 == 0) ? 8 : 1;
     const int64_t vecs = (K / cl + 7) / 8;
     // decode-sized M: as many threads as vectors (<= 2 per thread); large M: <= 4 per thread
     const int64_t want = M <= 64 ? (vecs + 1) / 2 : (vecs + 3) / 4;

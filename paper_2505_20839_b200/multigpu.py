@@ -147,6 +147,9 @@ def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src, clock_c
     ms2 = torch.tensor([e2.elapsed_time(e3)], device=dev)
     dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
     e2e_us = float(ms2.item()) * 1e3 / steps
+    # BASELINE configs[3]: Llama2-70B FFN column-parallel at M = 16 and M = 16384
+    from .c4 import c4_figures
+    c4 = c4_figures(F, dev, stream, rank, world, comm) if not getattr(args, "no_c4", False) else None
     comm.destroy()
 
     # dominant kernel: this rank's gate_up shard GEMM alone (no collective), rotating copies
@@ -193,6 +196,8 @@ def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src, clock_c
         }
         if clocks:
             line["clocks"] = clocks.summary()
+        if c4:
+            line["c4_llama2_70b_ffn"] = c4
         hbm = peaks["hbm_gbs"]
         line["roofline"] = {"bound": "hbm", "kernel": f"fireq_w4a8_gemm gate_up shard M={M} N={Nl} K={D_MODEL} (per rank)",
                             "achieved": round(gu_bytes / gu_us / 1e3, 1), "peak": hbm, "unit": "GB/s",

@@ -17,7 +17,7 @@ def bits_of(t):
     return t.cpu().view(torch.int16).numpy().view(np.uint16)
 
 
-@pytest.mark.parametrize("M,K", [(16, 4096), (8, 11008), (3, 128)])
+@pytest.mark.parametrize("M,K", [(16, 4096), (8, 11008), (3, 128), (300, 1024), (100, 11008), (64, 256)])
 def test_quantize_act_transposed_bit_exact(fireq, M, K):
     xb = synth.activations(M, K, 31)
     X = synth.bits_to_torch(xb).to(DEV)
@@ -29,7 +29,7 @@ def test_quantize_act_transposed_bit_exact(fireq, M, K):
     assert np.array_equal(q2.cpu().numpy(), rq) and np.array_equal(bits_of(b2), nm.bf16_to_bits(rb))
 
 
-@pytest.mark.parametrize("M,K", [(16, 11008), (5, 256)])
+@pytest.mark.parametrize("M,K", [(16, 11008), (5, 256), (200, 1408)])
 def test_silu_mul_quantize(fireq, M, K):
     gb = synth.activations(M, K, 41)
     ub = synth.activations(M, K, 42)

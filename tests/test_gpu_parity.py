@@ -437,3 +437,13 @@ def test_cooperative_launch_same_result(fireq):
                        capture_output=True, text=True, timeout=240)
     assert r.returncode == 0, r.stdout + r.stderr
     assert torch.equal(torch.load(tmp), y)
+
+
+@pytest.mark.parametrize("M,N,K", [(16, 448 * 128, 512), (32, 300 * 128, 256)])
+def test_gemm_decode_tail_wave_split(fireq, M, N, K):
+    """Decode tiles beyond whole waves: 448 tiles = 3 waves of 148 + 4; the 4 remaining tiles
+    are split stream-K over all CTAs instead of forming a 4th wave."""
+    plan = fireq.gemm_plan(M, N, K)
+    assert plan["mode"] == "stream-k" and plan["ctas"] == 148, plan
+    y, r, *_ = run_case(fireq, M, N, K, seed=N + 7)
+    assert og.g4_error(y, r) <= G4_TOL
