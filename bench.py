@@ -668,7 +668,7 @@ def main():
     if dist_on:
         # NCCL may print its version on stdout; the bench's stdout is ONE JSON line
         if not os.environ.get("FIREQ_KEEP_NCCL_DEBUG"):
-            os.environ["NCCL_DEBUG"] = "WARN"
+            os.environ["NCCL_DEBUG"] = "NONE"
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         os.environ.setdefault("RANK", str(rank))

@@ -238,6 +238,44 @@ fireq_status_t fireq_w4a8_gemm_colpar(const uint8_t* x_fp8, const void* x_scale,
                                       void* Yt_full, void* workspace, size_t workspace_bytes,
                                       fireq_comm_t comm, void* stream);
 
+/* ------------------------------ comm-fused column parallelism (NVLink, CUDA IPC) */
+/*
+ * A symmetric buffer is one device allocation per rank, same size on every rank:
+ *   [256 B: epoch flags, one u32 per source rank][Y^T data, nranks * N_local * M bf16]
+ * Each rank exports the IPC handle of its buffer (fireq_symm_handle: handle of the containing
+ * allocation + the buffer's offset in it), exchanges handles and offsets by any host means,
+ * and opens the group (fireq_symm_open maps every peer's buffer; nranks <= 8, one GPU
+ * per process; peers on the same node).  The flags must be zero before the first use.
+ */
+typedef struct fireq_symm* fireq_symm_t;
+/* bytes of a symmetric buffer holding data_bytes of Y^T (256 + data_bytes). */
+size_t fireq_symm_bytes(int64_t data_bytes);
+/* host: the IPC handle (64 bytes) of the allocation containing `buffer` and the buffer's byte
+ * offset inside it (allocators hand out interior pointers). */
+fireq_status_t fireq_symm_handle(void* buffer, uint8_t handle[64], int64_t* offset);
+/* host: handles [nranks][64] (entry `rank` ignored), offsets [nranks] of each rank's buffer
+ * inside the allocation its handle names (NULL = 0); local_buffer 16-B aligned. */
+fireq_status_t fireq_symm_open(fireq_symm_t* out, int nranks, int rank, void* local_buffer, size_t bytes,
+                               const uint8_t* handles, const int64_t* offsets);
+/* host: synchronizes the device, unmaps the peers' buffers, frees the handle. */
+fireq_status_t fireq_symm_close(fireq_symm_t symm);
+/*
+ * fireq_w4a8_gemm_colpar_p2p -- the column-parallel layer with the all-gather fused into the
+ * GEMM epilogue: this rank's Y^T slice [rank*N_local, (rank+1)*N_local) x M is
+ * stored by the epilogue straight into the same slot of EVERY rank's symmetric buffer (NVLink
+ * stores), then a one-CTA kernel advances the buffer's call counter, publishes it in every
+ * peer's flag area (release, system scope) and waits for all peers' flags to reach it
+ * (acquire): on return (stream order) the local buffer's Y^T [nranks*N_local][M] (data at
+ * offset 256, ld = M) is complete.  No NCCL.  Every rank must make the same sequence of calls
+ * on a buffer (the epochs then agree; CUDA-graph replays advance them on the device).
+ * Other arguments as fireq_w4a8_gemm_colpar.  Same values as the NCCL path, bit for bit.
+ */
+fireq_status_t fireq_w4a8_gemm_colpar_p2p(const uint8_t* x_fp8, const void* x_scale, int64_t M, int64_t K,
+                                          const uint8_t* w_packed_local, const uint8_t* w_scales_local,
+                                          int64_t N_local, int32_t pts_exponent,
+                                          const float* out_chan_scale_local, fireq_symm_t symm,
+                                          void* workspace, size_t workspace_bytes, void* stream);
+
 /* --------------------------------------------------------- introspection */
 /* Debug/test: writes the 127 x 16 LUT-of-LUTs the GEMM builds on chip
  * (entry [s][u] = E4M3_RN(v(u) * dec(s)), v(u) = u < 8 ? u : u - 16) into the

@@ -7,6 +7,8 @@ Per P (= world size) and M it reports, from rank 0 (times are max over ranks):
                  replicated activation quantizers, without the collectives
   gemm_ag_us     the full column-parallel FFN step: the same kernels plus the two in-place
                  NCCL all-gathers of Y^T (fireq_w4a8_gemm_colpar)
+  gemm_p2p_us    the step with the gathers fused into the GEMM epilogues (NVLink stores into
+                 every rank's symmetric buffer + epoch flags, fireq_w4a8_gemm_colpar_p2p)
   ag_busbw_gbs   the two all-gathers alone (same sizes, NCCL): bus bandwidth
                  bytes * (P - 1) / P / time
   vs_p1          rank 0 computes the single-GPU FFN output from the full weights (every rank
@@ -51,7 +53,7 @@ def _g4(y, r):
     return float(np.max(np.abs(y - r) / np.where(den > 0, den, 1.0)))
 
 
-def c4_figures(F, dev, stream, rank, world, comm=None, Ms=(16, 16384)):
+def c4_figures(F, dev, stream, rank, world, comm=None, Ms=(16, 16384), exchange=None):
     import synth
     wg = synth.weights(D_FF, D_MODEL, synth.layer_seed(3, 0))
     wu = synth.weights(D_FF, D_MODEL, synth.layer_seed(3, 1))
@@ -103,9 +105,25 @@ def c4_figures(F, dev, stream, rank, world, comm=None, Ms=(16, 16384)):
 
         reps = 20 if M <= 64 else 3
         rec = {}
+        ex = exchange if exchange is not None else (lambda obj: [obj])
+        symm_gu = F.Symmetric(world, rank, pg_plan.N_local, M, ex, device=dev)
+        symm_d = F.Symmetric(world, rank, pd_plan.N_local, M, ex, device=dev)
+
+        def gemm_p2p():
+            F.quantize_act(x, chan_mul=q_gu.c, out=(xq, beta), stream=stream)
+            g = F.w4a8_gemm_colpar_p2p(xq, beta, pg, sg, pg_plan.N_local, n_gu, symm_gu, ws1, gamma_local=gamma_l,
+                                       stream=stream)
+            F.silu_mul_quantize_act_t(g[:D_FF], g[D_FF:2 * D_FF], M, D_FF, out=(hq, hbeta), stream=stream)
+            F.w4a8_gemm_colpar_p2p(hq, hbeta, pd, sd, pd_plan.N_local, n_d, symm_d, ws2, stream=stream)
+
         rec["gemm_only_us"] = round(_max_over_ranks(_events(stream, gemm_only, reps), dev, world), 2)
         if comm is not None:
             rec["gemm_ag_us"] = round(_max_over_ranks(_events(stream, gemm_ag, reps), dev, world), 2)
+        rec["gemm_p2p_us"] = round(_max_over_ranks(_events(stream, gemm_p2p, reps), dev, world), 2)
+        with torch.cuda.stream(stream):
+            gemm_p2p()
+        torch.cuda.synchronize()
+        p2p_y = symm_d.yt[:D_MODEL].clone()
         if world > 1:
             import torch.distributed as dist
 
@@ -143,6 +161,7 @@ def c4_figures(F, dev, stream, rank, world, comm=None, Ms=(16, 16384)):
             yg = yt[:D_MODEL]
             same = bool(torch.equal(yg, y1))
             rec["vs_p1_bitwise"] = same
+            rec["p2p_equals_nccl"] = bool(torch.equal(p2p_y, yg))
             if not same:
                 rows = torch.arange(0, M, max(1, M // 64), device=dev)
                 a = yg[:, rows].t().float().cpu().numpy().astype(np.float64)
@@ -150,6 +169,8 @@ def c4_figures(F, dev, stream, rank, world, comm=None, Ms=(16, 16384)):
                 rec["vs_p1_g4"] = round(_g4(a, b), 5)
             del ws_a, ws_b, g1, y1
         out[f"M{M}"] = rec
-        del x, xq, gut, hq, yt, ws1, ws2
+        symm_gu.close()
+        symm_d.close()
+        del x, xq, gut, hq, yt, ws1, ws2, p2p_y
         torch.cuda.empty_cache()
     return out

@@ -3,6 +3,7 @@
 // column-parallel layer.  NCCL is resolved at run time with dlopen("libnccl.so.2")
 // so the library shares the NCCL already loaded by the host process (torch).
 #include <dlfcn.h>
+#include <cuda.h>
 #include <nvtx3/nvToolsExt.h>
 #include <cstring>
 #include <mutex>
@@ -26,7 +27,9 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
                          const uint8_t* w_packed, const uint8_t* w_scales, int64_t N, int32_t pts_n,
                          const float* gamma, __nv_bfloat16* Y, int64_t ldy, int out_layout, void* ws,
                          size_t ws_bytes, cudaStream_t stream, const void* pf0, size_t pf0_bytes,
-                         const void* pf1, size_t pf1_bytes);
+                         const void* pf1, size_t pf1_bytes, __nv_bfloat16* const* peers = nullptr,
+                         int npeer = 0);
+fireq_status_t symm_signal_wait(unsigned* const* flag_ptrs, int nranks, int rank, cudaStream_t stream);
 fireq_status_t debug_lut_table(uint8_t* out, cudaStream_t stream);
 size_t ffn_workspace_bytes(int64_t M, int64_t d_model, int64_t d_ff);
 bool ffn_shape_supported(int64_t M, int64_t d_model, int64_t d_ff);
@@ -217,7 +220,8 @@ static fireq_status_t gemm_checked(const uint8_t* x_fp8, const void* x_scale, in
                                    const uint8_t* w_packed, const uint8_t* w_scales, int64_t N, int32_t pts_exponent,
                                    const float* out_chan_scale, void* Y, int64_t ldy, int out_layout, void* workspace,
                                    size_t workspace_bytes, void* stream, const void* pf0, size_t pf0_bytes,
-                                   const void* pf1, size_t pf1_bytes) {
+                                   const void* pf1, size_t pf1_bytes, __nv_bfloat16* const* peers = nullptr,
+                                   int npeer = 0) {
     FIREQ_NVTX("fireq_w4a8_gemm");
     FIREQ_REQUIRE(x_fp8 && x_scale && w_packed && w_scales && Y && workspace, FIREQ_ERROR_INVALID_VALUE,
                   "fireq_w4a8_gemm: NULL required pointer");
@@ -237,7 +241,7 @@ static fireq_status_t gemm_checked(const uint8_t* x_fp8, const void* x_scale, in
                   "fireq_w4a8_gemm_prefetch: prefetch regions must be 16-byte aligned");
     return gemm_impl(x_fp8, static_cast<const __nv_bfloat16*>(x_scale), M, K, w_packed, w_scales, N, pts_exponent,
                      out_chan_scale, static_cast<__nv_bfloat16*>(Y), ldy, out_layout, workspace, workspace_bytes,
-                     static_cast<cudaStream_t>(stream), pf0, pf0_bytes, pf1, pf1_bytes);
+                     static_cast<cudaStream_t>(stream), pf0, pf0_bytes, pf1, pf1_bytes, peers, npeer);
 }
 
 fireq_status_t fireq_w4a8_gemm(const uint8_t* x_fp8, const void* x_scale, int64_t M, int64_t K,
@@ -433,4 +437,121 @@ fireq_status_t fireq_w4a8_gemm_colpar(const uint8_t* x_fp8, const void* x_scale,
     return FIREQ_SUCCESS;
 }
 
+
+// ------------------------------------------- comm-fused column parallelism (CUDA IPC)
+// Symmetric buffer: [flags: 64 x u32 (one per source rank), padded to 256 B][Y^T data].
+struct fireq_symm {
+    int nranks = 0, rank = 0;
+    void* local = nullptr;
+    size_t bytes = 0;
+    void* base[8] = {};            // every rank's buffer mapped into this process (base[rank] = local)
+    void* raw[8] = {};             // the pointers cudaIpcOpenMemHandle returned
+    bool opened[8] = {};
+    unsigned** d_flags = nullptr;  // device array of the nranks flag areas
+};
+
+size_t fireq_symm_bytes(int64_t data_bytes) { return data_bytes > 0 ? (size_t)(256 + data_bytes) : 0; }
+
+typedef CUresult (*PFN_memGetAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+fireq_status_t fireq_symm_handle(void* buffer, uint8_t handle[64], int64_t* offset) {
+    FIREQ_REQUIRE(buffer && handle && offset, FIREQ_ERROR_INVALID_VALUE, "fireq_symm_handle: NULL pointer");
+    // the IPC handle names the whole allocation (a caching allocator hands out interior pointers):
+    // report the buffer's offset inside it
+    static PFN_memGetAddressRange range = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            range = reinterpret_cast<PFN_memGetAddressRange>(p);
+    });
+    FIREQ_REQUIRE(range, FIREQ_ERROR_CUDA, "fireq_symm_handle: cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, reinterpret_cast<CUdeviceptr>(buffer)) != CUDA_SUCCESS)
+        return fail(FIREQ_ERROR_CUDA, "fireq_symm_handle: cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+    if (e != cudaSuccess) return fail(FIREQ_ERROR_CUDA, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    memcpy(handle, &h, 64);
+    *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(buffer) - base);
+    return FIREQ_SUCCESS;
+}
+
+fireq_status_t fireq_symm_open(fireq_symm_t* out, int nranks, int rank, void* local_buffer, size_t bytes,
+                               const uint8_t* handles, const int64_t* offsets) {
+    FIREQ_NVTX("fireq_symm_open");
+    FIREQ_REQUIRE(out && local_buffer && handles && nranks >= 1 && nranks <= 8 && rank >= 0 && rank < nranks &&
+                      bytes > 256,
+                  FIREQ_ERROR_INVALID_VALUE, "fireq_symm_open: bad arguments (1 <= nranks <= 8)");
+    FIREQ_REQUIRE(aligned16(local_buffer), FIREQ_ERROR_MISALIGNED, "fireq_symm_open: buffer must be 16-byte aligned");
+    fireq_symm* sy = new fireq_symm();
+    sy->nranks = nranks;
+    sy->rank = rank;
+    sy->local = local_buffer;
+    sy->bytes = bytes;
+    for (int q = 0; q < nranks; ++q) {
+        if (q == rank) {
+            sy->base[q] = local_buffer;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, handles + 64 * q, 64);
+        void* p = nullptr;
+        const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            for (int z = 0; z < q; ++z)
+                if (sy->opened[z]) cudaIpcCloseMemHandle(sy->raw[z]);
+            delete sy;
+            return fail(FIREQ_ERROR_CUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+        }
+        // the handle names the whole allocation; the buffer may start at an offset inside it
+        sy->raw[q] = p;
+        sy->base[q] = static_cast<uint8_t*>(p) + (offsets ? offsets[q] : 0);
+        sy->opened[q] = true;
+    }
+    unsigned* hf[8];
+    for (int q = 0; q < nranks; ++q) hf[q] = static_cast<unsigned*>(sy->base[q]);
+    if (cudaMalloc(&sy->d_flags, sizeof(unsigned*) * nranks) != cudaSuccess ||
+        cudaMemcpy(sy->d_flags, hf, sizeof(unsigned*) * nranks, cudaMemcpyHostToDevice) != cudaSuccess) {
+        delete sy;
+        return fail(FIREQ_ERROR_CUDA, "fireq_symm_open: flag table");
+    }
+    *out = sy;
+    return FIREQ_SUCCESS;
+}
+
+fireq_status_t fireq_symm_close(fireq_symm_t sy) {
+    FIREQ_REQUIRE(sy, FIREQ_ERROR_NOT_INITIALIZED, "fireq_symm_close: NULL handle");
+    cudaDeviceSynchronize();
+    for (int q = 0; q < sy->nranks; ++q)
+        if (sy->opened[q]) cudaIpcCloseMemHandle(sy->raw[q]);
+    if (sy->d_flags) cudaFree(sy->d_flags);
+    delete sy;
+    return FIREQ_SUCCESS;
+}
+
+fireq_status_t fireq_w4a8_gemm_colpar_p2p(const uint8_t* x_fp8, const void* x_scale, int64_t M, int64_t K,
+                                          const uint8_t* w_packed_local, const uint8_t* w_scales_local,
+                                          int64_t N_local, int32_t pts_exponent, const float* out_chan_scale_local,
+                                          fireq_symm_t symm, void* workspace, size_t workspace_bytes, void* stream) {
+    FIREQ_NVTX("fireq_w4a8_gemm_colpar_p2p");
+    FIREQ_REQUIRE(symm, FIREQ_ERROR_NOT_INITIALIZED, "fireq_w4a8_gemm_colpar_p2p: symmetric buffer not opened");
+    const size_t need = 256 + (size_t)symm->nranks * N_local * M * 2;
+    FIREQ_REQUIRE(symm->bytes >= need, FIREQ_ERROR_INVALID_VALUE, "fireq_w4a8_gemm_colpar_p2p: symmetric buffer too small");
+    __nv_bfloat16* dst[8];
+    for (int q = 0; q < symm->nranks; ++q)
+        dst[q] = reinterpret_cast<__nv_bfloat16*>(static_cast<uint8_t*>(symm->base[q]) + 256) +
+                 (size_t)symm->rank * N_local * M;
+    // the GEMM writes this rank's Y^T slice into every rank's buffer (NVLink stores), then every
+    // rank publishes its call count in each peer's flag area and waits for all peers' flags
+    fireq_status_t st = gemm_checked(x_fp8, x_scale, M, K, w_packed_local, w_scales_local, N_local, pts_exponent,
+                                     out_chan_scale_local, dst[symm->rank], M, 1, workspace, workspace_bytes, stream,
+                                     nullptr, 0, nullptr, 0, symm->nranks > 1 ? dst : nullptr, symm->nranks);
+    if (st != FIREQ_SUCCESS || symm->nranks == 1) return st;
+    return symm_signal_wait(symm->d_flags, symm->nranks, symm->rank, static_cast<cudaStream_t>(stream));
+}
 }  // extern "C"

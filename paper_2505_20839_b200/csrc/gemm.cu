@@ -51,6 +51,11 @@ struct GemmArgs {
     const __nv_bfloat16* x_scale;
     const float* gamma;
     __nv_bfloat16* Y;
+    // comm-fused column parallelism (out_layout 1): the Y^T tile is also stored to npeer - 1
+    // further destinations (this rank's slot of every peer's full Y^T, NVLink stores through
+    // CUDA-IPC mappings); Yp[0] == Y
+    __nv_bfloat16* Yp[8];
+    int npeer;
     float* partial;        // [2*C][NTOK][128] fp32 (stream-K only)
     unsigned* counters;    // [tiles]
     int64_t ldy;
@@ -671,12 +676,14 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             }
             const int mb = m0 + ch * 16;
             if (a.out_layout == 1) {
-                __nv_bfloat16* dst = a.Y + (size_t)n * a.ldy + mb;
-                if (mb + 16 <= a.M && (a.ldy & 7) == 0) {
-                    reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<const uint4*>(yb)[0];
-                    reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<const uint4*>(yb)[1];
-                } else {
-                    for (int c = 0; c < 16 && mb + c < a.M; ++c) dst[c] = yb[c];
+                for (int p = 0; p < (a.npeer > 1 ? a.npeer : 1); ++p) {
+                    __nv_bfloat16* dst = (a.npeer > 1 ? a.Yp[p] : a.Y) + (size_t)n * a.ldy + mb;
+                    if (mb + 16 <= a.M && (a.ldy & 7) == 0) {
+                        reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<const uint4*>(yb)[0];
+                        reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<const uint4*>(yb)[1];
+                    } else {
+                        for (int c = 0; c < 16 && mb + c < a.M; ++c) dst[c] = yb[c];
+                    }
                 }
             } else if (a.out_layout == 2) {
                 // SwiGLU pair (DESIGN R22): h = bf16(silu(g) * u) from the bf16-rounded gate and
@@ -1336,7 +1343,7 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
                          const uint8_t* w_packed, const uint8_t* w_scales, int64_t N, int32_t pts_n,
                          const float* gamma, __nv_bfloat16* Y, int64_t ldy, int out_layout, void* ws,
                          size_t ws_bytes, cudaStream_t stream, const void* pf0, size_t pf0_bytes,
-                         const void* pf1, size_t pf1_bytes) {
+                         const void* pf1, size_t pf1_bytes, __nv_bfloat16* const* peers, int npeer) {
     const Plan p = make_plan(M, N, K);
     if (ws_bytes < gemm_workspace_bytes(M, N, K)) return fail(FIREQ_ERROR_WORKSPACE, "GEMM workspace too small");
     CUtensorMap map;
@@ -1347,6 +1354,12 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
     args.Y = Y;
     args.ldy = ldy;
     args.out_layout = out_layout;
+    args.npeer = 0;
+    if (peers && npeer > 1) {
+        if (npeer > 8 || out_layout != 1) return fail(FIREQ_ERROR_INVALID_VALUE, "peer stores: Y^T and <= 8 ranks");
+        for (int q = 0; q < npeer; ++q) args.Yp[q] = peers[q];
+        args.npeer = npeer;
+    }
     switch (p.ntok) {
         // <NTOK, sign-split, converter WGs, SMEM stages, TMEM A stages, accumulators, groups/stage,
         //  MMA-issuing warps, resident activations>

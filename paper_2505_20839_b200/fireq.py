@@ -24,7 +24,8 @@ EXPORTS = [
     "fireq_w4a8_gemm_colpar", "fireq_debug_lut_table", "fireq_gemm_plan", "fireq_debug_set_trace",
     "fireq_quantize_act_t", "fireq_silu_mul_quantize_act_t", "fireq_debug_set_spans",
     "fireq_w4a8_gemm_prefetch", "fireq_interleave_gate_up", "fireq_ffn_workspace_bytes",
-    "fireq_ffn_w4a8_decode", "fireq_clear_cache",
+    "fireq_ffn_w4a8_decode", "fireq_clear_cache", "fireq_symm_bytes", "fireq_symm_handle", "fireq_symm_open",
+    "fireq_symm_close", "fireq_w4a8_gemm_colpar_p2p",
 ]
 
 
@@ -45,6 +46,11 @@ def load(path=LIB_PATH):
         "fireq_status_string": ([C], ctypes.c_char_p),
         "fireq_last_error": ([], ctypes.c_char_p),
         "fireq_clear_cache": ([], None),
+        "fireq_symm_bytes": ([I64], SZ),
+        "fireq_symm_handle": ([P, P, P], C),
+        "fireq_symm_open": ([P, C, C, P, SZ, P, P], C),
+        "fireq_symm_close": ([P], C),
+        "fireq_w4a8_gemm_colpar_p2p": ([P, P, I64, I64, P, P, I64, I32, P, P, P, SZ, P], C),
         "fireq_weight_layout_version": ([], C),
         "fireq_packed_weight_bytes": ([I64, I64], SZ),
         "fireq_weight_scale_bytes": ([I64, I64], SZ),
@@ -369,3 +375,50 @@ def w4a8_gemm_colpar(xq, beta, packed_local, scales_local, N_local, pts_n, comm,
                                         _stream(stream)),
            "fireq_w4a8_gemm_colpar")
     return Yt_full
+
+
+# ------------------------------------------------ comm-fused column parallelism (IPC)
+class Symmetric:
+    """A symmetric buffer (fireq_symm_*): [256 B flags][Y^T nranks*N_local x M bf16] on every rank,
+    peers mapped through CUDA IPC.  exchange(obj) -> list of every rank's obj (e.g. a
+    torch.distributed all_gather_object), used once for the handles."""
+
+    def __init__(self, nranks, rank, N_local, M, exchange, device="cuda"):
+        L = lib()
+        self.nranks, self.rank, self.N_local, self.M = nranks, rank, N_local, M
+        nbytes = L.fireq_symm_bytes(nranks * N_local * M * 2)
+        self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+        torch.cuda.synchronize(self.buf.device)
+        h = (ctypes.c_uint8 * 64)()
+        off = ctypes.c_int64()
+        _check(L.fireq_symm_handle(_ptr(self.buf), ctypes.cast(h, ctypes.c_void_p), ctypes.byref(off)),
+               "fireq_symm_handle")
+        allh = exchange((bytes(h), off.value))
+        hs = (ctypes.c_uint8 * (64 * nranks))()
+        offs = (ctypes.c_int64 * nranks)()
+        for q, (hq, oq) in enumerate(allh):
+            ctypes.memmove(ctypes.addressof(hs) + 64 * q, hq, 64)
+            offs[q] = oq
+        self.h = ctypes.c_void_p()
+        _check(L.fireq_symm_open(ctypes.byref(self.h), nranks, rank, _ptr(self.buf), nbytes,
+                                 ctypes.cast(hs, ctypes.c_void_p), ctypes.cast(offs, ctypes.c_void_p)),
+               "fireq_symm_open")
+        self.yt = self.buf[256:256 + nranks * N_local * M * 2].view(torch.bfloat16).view(nranks * N_local, M)
+
+    def close(self):
+        if self.h:
+            _check(lib().fireq_symm_close(self.h), "fireq_symm_close")
+            self.h = ctypes.c_void_p()
+
+
+def w4a8_gemm_colpar_p2p(xq, beta, packed_local, scales_local, N_local, pts_n, symm, workspace, gamma_local=None,
+                         stream=None):
+    """Column-parallel GEMM with the all-gather fused into the epilogue (NVLink stores into every
+    rank's symmetric buffer + device-side epoch flags; graph-capturable).  Returns symm.yt (the full Y^T) -- complete in stream order."""
+    M, K = xq.shape
+    ws = workspace.ensure(lib().fireq_w4a8_gemm_workspace_bytes(M, N_local, K), stream)
+    _check(lib().fireq_w4a8_gemm_colpar_p2p(_ptr(xq), _ptr(beta), M, K, _ptr(packed_local), _ptr(scales_local),
+                                            N_local, pts_n, _ptr(gamma_local), symm.h, _ptr(ws),
+                                            ws.numel(), _stream(stream)),
+           "fireq_w4a8_gemm_colpar_p2p")
+    return symm.yt

@@ -5,13 +5,15 @@ fireq_quantize_weight (deterministic, so CAS lambda and PTS n are identical on a
 ranks) and keeps its N-shard (sharding.py).  A decode step on rank r:
 
   fireq_quantize_act(x, c_gu)                         replicated (bit-identical on all ranks)
-  fireq_w4a8_gemm_colpar(W_gu shard r)  -> GU^T       rank's slice + in-place NCCL all-gather
+  fireq_w4a8_gemm_colpar_p2p(W_gu shard r) -> GU^T    the epilogue stores the rank's slice into
+                                                      every rank's symmetric buffer (NVLink)
   fireq_silu_mul_quantize_act_t(GU^T)                 replicated
-  fireq_w4a8_gemm_colpar(W_down shard r) -> Y^T       slice + in-place NCCL all-gather
+  fireq_w4a8_gemm_colpar_p2p(W_down shard r) -> Y^T   same
 
-The only data-path collectives are the two output all-gathers (north_star (d)); the
-communicator is libfireq's own NCCL communicator (unique id broadcast by torch.distributed,
-which is used for plumbing only: barriers and the max-over-ranks timing).
+The only data-path exchange is the output gather (north_star (d)), fused into the GEMM
+epilogue; the same step with the NCCL in-place all-gather
+(fireq_w4a8_gemm_colpar, libfireq's own NCCL communicator) is timed alongside.
+torch.distributed is plumbing only: handle exchange, barriers, max-over-ranks timing.
 """
 import json
 import os
@@ -55,6 +57,13 @@ def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src, clock_c
         pg, sg = sharding.shard_quantized(q_gu.packed, q_gu.scales, plan_gu, rank, D_MODEL, zeros_u8)
         pd, sd = sharding.shard_quantized(q_d.packed, q_d.scales, plan_d, rank, D_FF, zeros_u8)
         rot.append((pg, sg, pd, sd))
+    def exchange(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    symm_gu = F.Symmetric(world, rank, plan_gu.N_local, M, exchange, device=dev)
+    symm_d = F.Symmetric(world, rank, plan_d.N_local, M, exchange, device=dev)
     x = synth.bits_to_torch(synth.activations(M, D_MODEL, synth.layer_seed(1, 3))).to(dev)
     xq = torch.empty((M, D_MODEL), dtype=torch.uint8, device=dev)
     beta = torch.empty(M, dtype=torch.bfloat16, device=dev)
@@ -65,13 +74,21 @@ def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src, clock_c
     ws1 = F.Workspace(F.gemm_workspace_bytes(M, plan_gu.N_local, D_MODEL), dev)
     ws2 = F.Workspace(F.gemm_workspace_bytes(M, plan_d.N_local, D_FF), dev)
 
-    def step(r):
+    def step_nccl(r):
         pg, sg, pd, sd = rot[r]
         F.quantize_act(x, chan_mul=q_gu.c, out=(xq, beta), stream=stream)
         F.w4a8_gemm_colpar(xq, beta, pg, sg, plan_gu.N_local, n_gu, comm, gut, ws1, gamma_local=gamma_l,
                            stream=stream)
         F.silu_mul_quantize_act_t(gut[:D_FF], gut[D_FF:2 * D_FF], M, D_FF, out=(hq, hbeta), stream=stream)
         F.w4a8_gemm_colpar(hq, hbeta, pd, sd, plan_d.N_local, n_d, comm, yt, ws2, stream=stream)
+
+    def step(r):
+        pg, sg, pd, sd = rot[r]
+        F.quantize_act(x, chan_mul=q_gu.c, out=(xq, beta), stream=stream)
+        g = F.w4a8_gemm_colpar_p2p(xq, beta, pg, sg, plan_gu.N_local, n_gu, symm_gu, ws1, gamma_local=gamma_l,
+                                   stream=stream)
+        F.silu_mul_quantize_act_t(g[:D_FF], g[D_FF:2 * D_FF], M, D_FF, out=(hq, hbeta), stream=stream)
+        F.w4a8_gemm_colpar_p2p(hq, hbeta, pd, sd, plan_d.N_local, n_d, symm_d, ws2, stream=stream)
 
     with torch.cuda.stream(stream):
         for r in range(R):
@@ -128,7 +145,7 @@ def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src, clock_c
     def e2e_step(r):
         x.copy_(x_host, non_blocking=True)
         step(r)
-        y_host.copy_(yt, non_blocking=True)
+        y_host.copy_(symm_d.yt, non_blocking=True)
 
     with torch.cuda.stream(stream):
         for r in range(R):
@@ -147,10 +164,42 @@ def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src, clock_c
     ms2 = torch.tensor([e2.elapsed_time(e3)], device=dev)
     dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
     e2e_us = float(ms2.item()) * 1e3 / steps
+
+    # the same step with the NCCL in-place all-gathers (fireq_w4a8_gemm_colpar), for comparison
+    nccl_us = None
+    try:
+        g_n = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            for r in range(R):
+                step_nccl(r)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g_n, stream=stream):
+            for r in range(R):
+                step_nccl(r)
+        with torch.cuda.stream(stream):
+            g_n.replay()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e6, e7 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e6.record(stream)
+            for _ in range(calls):
+                g_n.replay()
+            e7.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        ms3 = torch.tensor([e6.elapsed_time(e7)], device=dev)
+        dist.all_reduce(ms3, op=dist.ReduceOp.MAX)
+        nccl_us = float(ms3.item()) * 1e3 / steps
+        del g_n
+    except Exception as e:
+        print(f"[rank {rank}] NCCL comparison skipped: {e}", file=sys.stderr)
     # BASELINE configs[3]: Llama2-70B FFN column-parallel at M = 16 and M = 16384
     from .c4 import c4_figures
-    c4 = c4_figures(F, dev, stream, rank, world, comm) if not getattr(args, "no_c4", False) else None
+    c4 = c4_figures(F, dev, stream, rank, world, comm, exchange=exchange) if not getattr(args, "no_c4", False) else None
     comm.destroy()
+    symm_gu.close()
+    symm_d.close()
 
     # dominant kernel: this rank's gate_up shard GEMM alone (no collective), rotating copies
     gu_out = torch.empty((M, plan_gu.N_local), dtype=torch.bfloat16, device=dev)
@@ -188,7 +237,8 @@ def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src, clock_c
             "ms_per_step": round(us_per_step / 1e3, 6), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "fp8e4m3 x int4 -> f32 acc -> bf16", "data": "synthetic",
             "config": {"workload": "llama2-7b-ffn-decode-b16", "tokens": M, "d_model": D_MODEL, "d_ff": D_FF,
-                       "parallelism": f"column-parallel tp{world} (N-sharded gate_up + down, NCCL all-gather of Y^T)",
+                       "parallelism": f"column-parallel tp{world} (N-sharded gate_up + down; Y^T gathered by the "
+                                      "GEMM epilogue's NVLink stores into every rank's buffer, CUDA IPC)",
                        "l2": f"{R} rotating weight-shard copies", "graph": "captured" if graphed else "eager"},
             "gpu_launches": 4 * steps,
             "e2e": {"value": round(e2e_us, 3), "unit": "us", "h2d_bytes_per_step": x.numel() * 2,
@@ -198,6 +248,8 @@ def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src, clock_c
             line["clocks"] = clocks.summary()
         if c4:
             line["c4_llama2_70b_ffn"] = c4
+        if nccl_us is not None:
+            line["nccl_allgather_variant_us"] = round(nccl_us, 3)
         hbm = peaks["hbm_gbs"]
         line["roofline"] = {"bound": "hbm", "kernel": f"fireq_w4a8_gemm gate_up shard M={M} N={Nl} K={D_MODEL} (per rank)",
                             "achieved": round(gu_bytes / gu_us / 1e3, 1), "peak": hbm, "unit": "GB/s",

@@ -93,3 +93,107 @@ def test_shards_decode_vs_oracle(fireq, P, N):
     yf = full.t().float().cpu().numpy().astype(np.float64)
     assert og.g4_error(y, r) <= 1e-2
     assert og.g4_error(y, yf) <= 1e-2
+
+
+# ----------------------------------------------- comm-fused column parallelism (f2)
+def test_colpar_p2p_world1(fireq):
+    """fireq_w4a8_gemm_colpar_p2p at one rank: the epilogue's Y^T in the symmetric buffer equals the
+    plain GEMM's Y^T bit for bit (no signalling at world size 1)."""
+    M, N, K = 16, 1024, 2048
+    _, _, qw, xq, beta = _setup(fireq, M, N, K, 1601)
+    symm = fireq.Symmetric(1, 0, N, M, exchange=lambda obj: [obj])
+    try:
+        ws = fireq.Workspace(fireq.gemm_workspace_bytes(M, N, K))
+        yt = fireq.w4a8_gemm_colpar_p2p(xq, beta, qw.packed, qw.scales, N, qw.n, symm, ws)
+        ref = fireq.w4a8_gemm(xq, beta, qw.packed, qw.scales, N, qw.n, out_layout=1)
+        torch.cuda.synchronize()
+        assert torch.equal(yt, ref)
+    finally:
+        symm.close()
+
+
+def _p2p_rank(rank, world, port, M, N, K, out_dir):
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    from paper_2505_20839_b200 import fireq as F
+    from paper_2505_20839_b200 import sharding as sh
+    F.load()
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        wb = synth.weights(N, K, 1701)
+        xb = synth.activations(M, K, 1702)
+        qw = F.quantize_weight(synth.bits_to_torch(wb).cuda(), cas_mode=1)
+        xq, beta = F.quantize_act(synth.bits_to_torch(xb).cuda(), chan_mul=qw.c)
+        plan = sh.ShardPlan(N, world)
+        pl, sl = sh.shard_quantized(qw.packed, qw.scales, plan, rank, K,
+                                    lambda n: torch.zeros(n, dtype=torch.uint8, device="cuda"))
+
+        def exchange(obj):
+            out = [None] * world
+            dist.all_gather_object(out, obj)
+            return out
+
+        symm = F.Symmetric(world, rank, plan.N_local, M, exchange)
+        ws = F.Workspace(F.gemm_workspace_bytes(M, plan.N_local, K))
+        ref = F.w4a8_gemm(xq, beta, qw.packed, qw.scales, N, qw.n, out_layout=1)
+        s = torch.cuda.Stream()
+        ok = []
+        for it in range(3):                       # repeated calls: the epochs advance
+            with torch.cuda.stream(s):
+                symm.yt.zero_()
+                dist.barrier()
+                yt = F.w4a8_gemm_colpar_p2p(xq, beta, pl, sl, plan.N_local, qw.n, symm, ws, stream=s)
+            torch.cuda.synchronize()
+            ok.append(yt[:N].clone())
+            dist.barrier()
+        # graph capture: replays advance the device-side epochs
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            F.w4a8_gemm_colpar_p2p(xq, beta, pl, sl, plan.N_local, qw.n, symm, ws, stream=s)
+        for it in range(2):
+            symm.yt.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            g.replay()
+            torch.cuda.synchronize()
+            ok.append(symm.yt[:N].clone())
+            dist.barrier()
+        whole = F.gemm_plan(M, N, K)["mode"] == "tiles" and F.gemm_plan(M, plan.N_local, K)["mode"] == "tiles"
+        res = []
+        for y in ok:
+            if whole:
+                res.append(bool(torch.equal(y, ref)))
+            else:
+                a = y.t().float().cpu().numpy().astype(np.float64)
+                b = ref.t().float().cpu().numpy().astype(np.float64)
+                res.append(og.g4_error(a, b) <= 1e-2 and not torch.isnan(y.float()).any().item())
+        symm.close()
+        with open(os.path.join(out_dir, f"rank{rank}.txt"), "w") as f:
+            f.write("ok" if all(res) else f"fail {res}")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("M,N,K", [(16, 3072, 1024), (8192, 4096, 256)])
+def test_colpar_p2p_two_ranks_one_gpu(fireq, tmp_path, M, N, K):
+    """Two processes on one GPU (CUDA IPC works between processes of the same device): each rank's
+    epilogue stores its Y^T slice into both symmetric buffers and the flags complete the exchange;
+    both ranks hold the single-GPU Y^T (bitwise for whole-tile plans, else G4), across repeated
+    calls and CUDA-graph replays."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_p2p_rank, args=(r, 2, port, M, N, K, str(tmp_path))) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    for r in range(2):
+        assert (tmp_path / f"rank{r}.txt").read_text() == "ok"
