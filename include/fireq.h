@@ -238,6 +238,31 @@ fireq_status_t fireq_w4a8_gemm_colpar(const uint8_t* x_fp8, const void* x_scale,
                                       void* Yt_full, void* workspace, size_t workspace_bytes,
                                       fireq_comm_t comm, void* stream);
 
+/* ------------------------------------------------- sigma_BF16 comparison variant */
+/*
+ * The paper's comparison point with BF16 group scales (App. B.1; DESIGN
+ * reading R25): W1-W3 as fireq_quantize_weight (CAS lambda, PTS n), then per 128-group
+ * sigma = bf16_RN(max|W_tilde| / 7) and codes = clamp(RNE(W_tilde / sigma), -8, 7) (sigma = 0
+ * -> 0).  Codes in layout v1; scales bf16 [N/128][K/128][128] (N*K/64 bytes).
+ */
+size_t fireq_weight_scale_bytes_bf16s(int64_t N, int64_t K);
+fireq_status_t fireq_quantize_weight_bf16s(const void* W, int64_t N, int64_t K, int cas_mode,
+                                           uint8_t* w_packed, void* w_scales_bf16, float* cas_lambda,
+                                           void* cas_inv, int32_t* pts_and_status, void* workspace,
+                                           size_t workspace_bytes, void* stream);
+/* Device workspace of fireq_w4a8_gemm_bf16s (FP32 split-K partials). */
+size_t fireq_w4a8_gemm_bf16s_workspace_bytes(int64_t M, int64_t N, int64_t K);
+/*
+ * fireq_w4a8_gemm_bf16s -- y[m][n] = bf16_RN(beta_m 2^-n sum_g sigma_{n,g} * P_g[m][n]) with
+ * P_g = sum_{k in g} dec(x_fp8[m][k]) * code[n][k] on the FP8 tensor cores (codes are exact
+ * E4M3 integers) and the per-group scaling + accumulation in FP32 on CUDA cores.  Row-major Y
+ * [M][ldy], ldy >= N.  Tolerance-checked against the oracle (G4).
+ */
+fireq_status_t fireq_w4a8_gemm_bf16s(const uint8_t* x_fp8, const void* x_scale, int64_t M, int64_t K,
+                                     const uint8_t* w_packed, const void* w_scales_bf16, int64_t N,
+                                     int32_t pts_exponent, void* Y, int64_t ldy, void* workspace,
+                                     size_t workspace_bytes, void* stream);
+
 /* ------------------------------ comm-fused column parallelism (NVLink, CUDA IPC) */
 /*
  * A symmetric buffer is one device allocation per rank, same size on every rank:

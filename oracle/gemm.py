@@ -63,6 +63,14 @@ def reference_rows(x_codes, beta, w_deq_rows, pts_n, gamma_rows=None):
     return r
 
 
+def gemm_reference_bf16s(x_codes, beta, codes, sigma, pts_n):
+    """G2 for the sigma_BF16 variant: r = beta 2^-n sum_k dec(x_hat) * code * sigma_{n,g(k)} (fp64; the
+    products code * sigma are exact).  codes int [N][K], sigma float64 [N][K/128]."""
+    x = E4M3_DECODE[np.asarray(x_codes, dtype=np.uint8)]
+    w = np.asarray(codes, dtype=np.float64) * np.repeat(np.asarray(sigma, dtype=np.float64), layout.GROUP, axis=1)
+    return (x @ w.T) * np.asarray(beta, dtype=np.float64)[:, None] * 2.0 ** (-pts_n)
+
+
 def g4_error(y, r):
     """G4: max over (m, n) of |y - r| / max(|r|, 0.1 * rms of row m of r)."""
     y = np.asarray(y, dtype=np.float64)

@@ -79,6 +79,16 @@ def pack_scales(scale_codes):
     return out
 
 
+def pack_scales16(scale_bits):
+    """sigma_BF16 bit patterns uint16 [N][K/128] -> blocked uint16 [N*K/128] (same block order)."""
+    sc = np.asarray(scale_bits, dtype=np.uint16)
+    N, G = sc.shape
+    n, g = np.meshgrid(np.arange(N), np.arange(G), indexing="ij")
+    out = np.zeros(N * G, dtype=np.uint16)
+    out[scale_index(n, g, G * GROUP)] = sc
+    return out
+
+
 def unpack_scales(blocked, N, K):
     G = K // GROUP
     n, g = np.meshgrid(np.arange(N), np.arange(G), indexing="ij")

@@ -197,6 +197,40 @@ def quantize_weight(W, cas_mode, pack=True, rows=None):
                            scales=layout.pack_scales(sigma_codes) if pack else None)
 
 
+# ---------------------------------------------------------- sigma_BF16 variant
+def quantize_weight_bf16s(W, cas_mode, pack=True, rows=None):
+    """The paper's comparison variant with BF16 group scales (P:316, App. B.1 P:525-527;
+    DESIGN reading R25): W1-W3 unchanged (CAS, PTS), then per 128-group
+
+      sigma = bf16_RN(max|W_tilde| / 7)        (no toward-zero step: Lemma 1 concerns FP8)
+      code  = clamp(RNE(W_tilde / sigma), -8, 7),  sigma = 0 -> 0
+
+    The dequantized weight is code * sigma exactly (no FP8 re-rounding).  Returns the fields of
+    quantize_weight with sigma_bits (uint16 [N][G]) and scales16 (blocked uint16, layout v1
+    order) in place of the FP8 codes.
+    """
+    W = np.asarray(W, dtype=np.float64)
+    N, K = W.shape
+    if N % layout.TILE_N or K % GROUP:
+        raise ValueError("N and K must be multiples of 128")
+    lam, c = cas_lambda(W, cas_mode)
+    W_bar = cas_apply(W, lam)
+    n, reason = pts_exponent(W_bar)
+    if rows is not None:
+        if pack:
+            raise ValueError("rows= needs pack=False")
+        W_bar = W_bar[np.asarray(rows)]
+    W_tilde = W_bar * 2.0 ** n
+    Nr = W_tilde.shape[0]
+    m = np.abs(W_tilde).reshape(Nr, K // GROUP, GROUP).max(axis=2)
+    sigma = bf16_rn(m / 7.0)
+    codes = group_codes(W_tilde.reshape(Nr, K // GROUP, GROUP), sigma[:, :, None]).reshape(Nr, K)
+    sigma_bits = (sigma.astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    return QuantizedWeight(lam=lam, c=c, n=n, reason=reason, sigma=sigma, sigma_bits=sigma_bits, codes=codes,
+                           packed=layout.pack_codes(codes) if pack else None,
+                           scales16=layout.pack_scales16(sigma_bits) if pack else None)
+
+
 # ------------------------------------------------------------------- A1 .. A3
 def quantize_act(X, c=None):
     """A1-A3 for X bf16 [M][K] (float64 array of bf16 values).

@@ -16,7 +16,11 @@ namespace fireq {
 // implemented in the kernel translation units
 fireq_status_t quantize_weight_impl(const __nv_bfloat16* W, int64_t N, int64_t K, int cas_mode, uint8_t* w_packed,
                                     uint8_t* w_scales, float* cas_lambda, __nv_bfloat16* cas_inv,
-                                    int32_t* pts_and_status, void* ws, cudaStream_t stream);
+                                    int32_t* pts_and_status, void* ws, cudaStream_t stream, bool bf16_scales);
+size_t gemm_bf16s_workspace_bytes(int64_t M, int64_t N, int64_t K);
+fireq_status_t gemm_bf16s_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int64_t M, int64_t K,
+                               const uint8_t* w_packed, const uint16_t* w_scales, int64_t N, int32_t pts_n,
+                               __nv_bfloat16* Y, int64_t ldy, void* ws, size_t ws_bytes, cudaStream_t stream);
 size_t wq_workspace_bytes(int64_t K);
 fireq_status_t quantize_act_impl(const __nv_bfloat16* X, const __nv_bfloat16* U, int64_t M, int64_t K, int64_t ld,
                                  const __nv_bfloat16* c, int mode, bool transposed, uint8_t* xq,
@@ -131,10 +135,9 @@ size_t fireq_w4a8_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
     return gemm_workspace_bytes(M, N, K);
 }
 
-fireq_status_t fireq_quantize_weight(const void* W, int64_t N, int64_t K, int cas_mode, uint8_t* w_packed,
+static fireq_status_t quantize_weight_checked(const void* W, int64_t N, int64_t K, int cas_mode, uint8_t* w_packed,
                                      uint8_t* w_scales, float* cas_lambda, void* cas_inv, int32_t* pts_and_status,
-                                     void* workspace, size_t workspace_bytes, void* stream) {
-    FIREQ_NVTX("fireq_quantize_weight");
+                                     void* workspace, size_t workspace_bytes, void* stream, bool bf16) {
     FIREQ_REQUIRE(W && w_packed && w_scales && pts_and_status, FIREQ_ERROR_INVALID_VALUE,
                   "fireq_quantize_weight: NULL required pointer");
     FIREQ_REQUIRE(cas_mode == 0 || cas_mode == 1, FIREQ_ERROR_INVALID_VALUE, "fireq_quantize_weight: cas_mode must be 0 or 1");
@@ -147,7 +150,53 @@ fireq_status_t fireq_quantize_weight(const void* W, int64_t N, int64_t K, int ca
                   "fireq_quantize_weight: workspace too small");
     return quantize_weight_impl(static_cast<const __nv_bfloat16*>(W), N, K, cas_mode, w_packed, w_scales, cas_lambda,
                                 static_cast<__nv_bfloat16*>(cas_inv), pts_and_status, workspace,
-                                static_cast<cudaStream_t>(stream));
+                                static_cast<cudaStream_t>(stream), bf16);
+}
+
+fireq_status_t fireq_quantize_weight(const void* W, int64_t N, int64_t K, int cas_mode, uint8_t* w_packed,
+                                     uint8_t* w_scales, float* cas_lambda, void* cas_inv, int32_t* pts_and_status,
+                                     void* workspace, size_t workspace_bytes, void* stream) {
+    FIREQ_NVTX("fireq_quantize_weight");
+    return quantize_weight_checked(W, N, K, cas_mode, w_packed, w_scales, cas_lambda, cas_inv, pts_and_status,
+                                   workspace, workspace_bytes, stream, false);
+}
+
+size_t fireq_weight_scale_bytes_bf16s(int64_t N, int64_t K) { return (N > 0 && K > 0) ? (size_t)(N * K / 64) : 0; }
+
+fireq_status_t fireq_quantize_weight_bf16s(const void* W, int64_t N, int64_t K, int cas_mode, uint8_t* w_packed,
+                                           void* w_scales_bf16, float* cas_lambda, void* cas_inv,
+                                           int32_t* pts_and_status, void* workspace, size_t workspace_bytes,
+                                           void* stream) {
+    FIREQ_NVTX("fireq_quantize_weight_bf16s");
+    FIREQ_REQUIRE(!w_scales_bf16 || aligned16(w_scales_bf16), FIREQ_ERROR_MISALIGNED,
+                  "fireq_quantize_weight_bf16s: w_scales must be 16-byte aligned");
+    return quantize_weight_checked(W, N, K, cas_mode, w_packed, static_cast<uint8_t*>(w_scales_bf16), cas_lambda,
+                                   cas_inv, pts_and_status, workspace, workspace_bytes, stream, true);
+}
+
+size_t fireq_w4a8_gemm_bf16s_workspace_bytes(int64_t M, int64_t N, int64_t K) {
+    if (M < 1 || N < 128 || K < 128) return 0;
+    return gemm_bf16s_workspace_bytes(M, N, K);
+}
+
+fireq_status_t fireq_w4a8_gemm_bf16s(const uint8_t* x_fp8, const void* x_scale, int64_t M, int64_t K,
+                                     const uint8_t* w_packed, const void* w_scales_bf16, int64_t N,
+                                     int32_t pts_exponent, void* Y, int64_t ldy, void* workspace,
+                                     size_t workspace_bytes, void* stream) {
+    FIREQ_NVTX("fireq_w4a8_gemm_bf16s");
+    FIREQ_REQUIRE(x_fp8 && x_scale && w_packed && w_scales_bf16 && Y && workspace, FIREQ_ERROR_INVALID_VALUE,
+                  "fireq_w4a8_gemm_bf16s: NULL required pointer");
+    FIREQ_REQUIRE(M >= 1 && M <= (int64_t(1) << 24), FIREQ_ERROR_INVALID_VALUE, "fireq_w4a8_gemm_bf16s: M in [1, 2^24]");
+    FIREQ_REQUIRE(pts_exponent >= 0 && pts_exponent <= 60, FIREQ_ERROR_INVALID_VALUE,
+                  "fireq_w4a8_gemm_bf16s: pts_exponent must be in [0, 60]");
+    FIREQ_REQUIRE(K >= 128 && K % 128 == 0 && K <= 65536 && N >= 128 && N % 128 == 0 && N <= (int64_t(1) << 20) &&
+                      (int64_t)M * N <= (int64_t(1) << 31),
+                  FIREQ_ERROR_UNSUPPORTED_SHAPE, "fireq_w4a8_gemm_bf16s: N, K multiples of 128");
+    FIREQ_REQUIRE(aligned16(x_fp8) && aligned16(w_packed) && aligned16(w_scales_bf16) && ldy >= N,
+                  FIREQ_ERROR_MISALIGNED, "fireq_w4a8_gemm_bf16s: 16-byte aligned operands, ldy >= N");
+    return gemm_bf16s_impl(x_fp8, static_cast<const __nv_bfloat16*>(x_scale), M, K, w_packed,
+                           static_cast<const uint16_t*>(w_scales_bf16), N, pts_exponent, static_cast<__nv_bfloat16*>(Y),
+                           ldy, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
 }
 
 static fireq_status_t check_act_args(const void* X, int64_t M, int64_t K, int64_t ldx, uint8_t* x_fp8,

@@ -142,6 +142,10 @@ __global__ void k_pts(WStats* st, int32_t* pts_and_status) {
 }
 
 // W4..W6: one warp per (row n, group g).  Lane l owns k = g*128 + 4l .. 4l+3.
+// BF16S: the sigma_BF16 variant (App. B.1; DESIGN reading R25): sigma =
+// bf16_RN(m / 7) (the fp32 quotient of an fp32 m by 7 is never moved onto a bf16 midpoint, so
+// this is the exact-rational RNE), stored as bf16 [N/128][K/128][128].
+template <bool BF16S>
 __global__ void k_group_quant_pack(const __nv_bfloat16* __restrict__ W, int64_t N, int64_t K,
                                    const float* __restrict__ lam, const WStats* __restrict__ st,
                                    uint8_t* __restrict__ packed, uint8_t* __restrict__ scales) {
@@ -164,9 +168,17 @@ __global__ void k_group_quant_pack(const __nv_bfloat16* __restrict__ W, int64_t 
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     // W4: sigma = largest E4M3 s with 7*s <= m.  RN(m/7) is at most one grid step
     // above it; 7*s is exact in fp32 (<= 7 significant bits), so compare exactly.
-    uint32_t sc = e4m3_rn(__fdiv_rn(m, 7.0f));
-    if (__fmul_rn(7.0f, e4m3_decode(sc)) > m) sc -= 1u;
-    const float sigma = e4m3_decode(sc);
+    uint32_t sc;
+    float sigma;
+    if (BF16S) {
+        const __nv_bfloat16 sb = __float2bfloat16_rn(__fdiv_rn(m, 7.0f));
+        sc = (uint32_t)__bfloat16_as_ushort(sb);
+        sigma = __bfloat162float(sb);
+    } else {
+        sc = e4m3_rn(__fdiv_rn(m, 7.0f));
+        if (__fmul_rn(7.0f, e4m3_decode(sc)) > m) sc -= 1u;
+        sigma = e4m3_decode(sc);
+    }
     // W5: codes
     uint32_t nib[4];
 #pragma unroll
@@ -184,7 +196,10 @@ __global__ void k_group_quant_pack(const __nv_bfloat16* __restrict__ W, int64_t 
     const int64_t off = (((nt * G + g) * 4 + j) * 128 + r) * 16 + b;
     const uint16_t two = (uint16_t)(nib[0] | (nib[1] << 4) | (nib[2] << 8) | (nib[3] << 12));
     *reinterpret_cast<uint16_t*>(packed + off) = two;
-    if (lane == 0) scales[(nt * G + g) * 128 + r] = (uint8_t)sc;
+    if (lane == 0) {
+        if (BF16S) reinterpret_cast<uint16_t*>(scales)[(nt * G + g) * 128 + r] = (uint16_t)sc;
+        else scales[(nt * G + g) * 128 + r] = (uint8_t)sc;
+    }
 }
 
 }  // namespace
@@ -196,7 +211,7 @@ size_t wq_workspace_bytes(int64_t K) {
 fireq_status_t quantize_weight_impl(const __nv_bfloat16* W, int64_t N, int64_t K, int cas_mode,
                                     uint8_t* w_packed, uint8_t* w_scales, float* cas_lambda,
                                     __nv_bfloat16* cas_inv, int32_t* pts_and_status, void* ws,
-                                    cudaStream_t stream) {
+                                    cudaStream_t stream, bool bf16_scales) {
     uint8_t* base = static_cast<uint8_t*>(ws);
     WStats* st = reinterpret_cast<WStats*>(base);
     float* absmean = reinterpret_cast<float*>(base + 256);
@@ -212,8 +227,11 @@ fireq_status_t quantize_weight_impl(const __nv_bfloat16* W, int64_t N, int64_t K
     k_wstats<<<blocks, 256, 0, stream>>>(W, total, K, lam, st);
     k_pts<<<1, 1, 0, stream>>>(st, pts_and_status);
     const int64_t warps = N * (K / 128);
-    k_group_quant_pack<<<(unsigned)((warps + 7) / 8), 256, 0, stream>>>(W, N, K, lam, st, w_packed, w_scales);
-    return check_launch("fireq_quantize_weight");
+    if (bf16_scales)
+        k_group_quant_pack<true><<<(unsigned)((warps + 7) / 8), 256, 0, stream>>>(W, N, K, lam, st, w_packed, w_scales);
+    else
+        k_group_quant_pack<false><<<(unsigned)((warps + 7) / 8), 256, 0, stream>>>(W, N, K, lam, st, w_packed, w_scales);
+    return check_launch(bf16_scales ? "fireq_quantize_weight_bf16s" : "fireq_quantize_weight");
 }
 
 // Row order of the fused FFN's gate_up weight: 128-row tile t

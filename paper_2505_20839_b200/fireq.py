@@ -25,7 +25,8 @@ EXPORTS = [
     "fireq_quantize_act_t", "fireq_silu_mul_quantize_act_t", "fireq_debug_set_spans",
     "fireq_w4a8_gemm_prefetch", "fireq_interleave_gate_up", "fireq_ffn_workspace_bytes",
     "fireq_ffn_w4a8_decode", "fireq_clear_cache", "fireq_symm_bytes", "fireq_symm_handle", "fireq_symm_open",
-    "fireq_symm_close", "fireq_w4a8_gemm_colpar_p2p",
+    "fireq_symm_close", "fireq_w4a8_gemm_colpar_p2p", "fireq_weight_scale_bytes_bf16s",
+    "fireq_quantize_weight_bf16s", "fireq_w4a8_gemm_bf16s_workspace_bytes", "fireq_w4a8_gemm_bf16s",
 ]
 
 
@@ -47,6 +48,10 @@ def load(path=LIB_PATH):
         "fireq_last_error": ([], ctypes.c_char_p),
         "fireq_clear_cache": ([], None),
         "fireq_symm_bytes": ([I64], SZ),
+        "fireq_weight_scale_bytes_bf16s": ([I64, I64], SZ),
+        "fireq_quantize_weight_bf16s": ([P, I64, I64, C, P, P, P, P, P, P, SZ, P], C),
+        "fireq_w4a8_gemm_bf16s_workspace_bytes": ([I64, I64, I64], SZ),
+        "fireq_w4a8_gemm_bf16s": ([P, P, I64, I64, P, P, I64, I32, P, I64, P, SZ, P], C),
         "fireq_symm_handle": ([P, P, P], C),
         "fireq_symm_open": ([P, C, C, P, SZ, P, P], C),
         "fireq_symm_close": ([P], C),
@@ -422,3 +427,35 @@ def w4a8_gemm_colpar_p2p(xq, beta, packed_local, scales_local, N_local, pts_n, s
                                             ws.numel(), _stream(stream)),
            "fireq_w4a8_gemm_colpar_p2p")
     return symm.yt
+
+
+# ------------------------------------------------------------ sigma_BF16 variant
+def quantize_weight_bf16s(W, cas_mode=1, stream=None):
+    """fireq_quantize_weight_bf16s: QuantizedWeight whose .scales are bf16 [N/128][K/128][128]."""
+    assert W.dtype == torch.bfloat16 and W.dim() == 2 and W.is_contiguous()
+    N, K = W.shape
+    dev = W.device
+    L = lib()
+    packed = torch.empty(L.fireq_packed_weight_bytes(N, K), dtype=torch.uint8, device=dev)
+    scales = torch.empty(N * K // 128, dtype=torch.bfloat16, device=dev)
+    lam = torch.empty(K, dtype=torch.float32, device=dev)
+    c = torch.empty(K, dtype=torch.bfloat16, device=dev)
+    ps = torch.empty(2, dtype=torch.int32, device=dev)
+    ws = _zeros_on(L.fireq_quantize_weight_workspace_bytes(N, K), dev, stream)
+    _check(L.fireq_quantize_weight_bf16s(_ptr(W), N, K, cas_mode, _ptr(packed), _ptr(scales), _ptr(lam), _ptr(c),
+                                         _ptr(ps), _ptr(ws), ws.numel(), _stream(stream)),
+           "fireq_quantize_weight_bf16s")
+    return QuantizedWeight(packed, scales, lam, c, ps, N, K)
+
+
+def w4a8_gemm_bf16s(xq, beta, packed, scales_bf16, N, pts_n, out=None, workspace=None, stream=None):
+    """Y = fireq_w4a8_gemm_bf16s(...): bf16 [M][N] (per-group scaled FP32 accumulation)."""
+    M, K = xq.shape
+    L = lib()
+    need = L.fireq_w4a8_gemm_bf16s_workspace_bytes(M, N, K)
+    ws = workspace.ensure(need, stream) if workspace is not None else _zeros_on(need, xq.device, stream)
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.bfloat16, device=xq.device)
+    _check(L.fireq_w4a8_gemm_bf16s(_ptr(xq), _ptr(beta), M, K, _ptr(packed), _ptr(scales_bf16), N, pts_n, _ptr(out),
+                                   out.stride(0), _ptr(ws), ws.numel(), _stream(stream)), "fireq_w4a8_gemm_bf16s")
+    return out

@@ -441,3 +441,77 @@ def test_quantize_weight_rows_subset_equals_full():
     assert np.array_equal(full.sigma_codes[rows], sub.sigma_codes)
     with pytest.raises(ValueError):
         oq.quantize_weight(W, 1, rows=rows)
+
+
+# ---------------------------------------------------------- sigma_BF16 variant (R25)
+def _bf16_rne_exact(q):
+    """Exact-rational round-to-nearest-even of a positive Fraction onto the bf16 grid (normal range)."""
+    if q == 0:
+        return Fraction(0)
+    e = 0
+    while q >= 2:
+        q /= 2
+        e += 1
+    while q < 1:
+        q *= 2
+        e -= 1
+    # q in [1, 2): 7 fraction bits
+    scaled = q * 128
+    lo = scaled.numerator // scaled.denominator
+    rem = scaled - lo
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and lo % 2 == 1):
+        lo += 1
+    return Fraction(lo, 128) * (Fraction(2) ** e)
+
+
+def test_bf16s_sigma_is_exact_rational_rne():
+    """sigma_BF16 = bf16_RN(m / 7): the float64 division then bf16 rounding equals the exact
+    rational RNE (no double rounding), on random fp32 group maxima and on m = 7 x bf16 midpoints."""
+    rng = np.random.default_rng(2501)
+    ms = list(nm.f32(np.exp(rng.uniform(-20, 6, 3000))))
+    for v in [1.00390625, 1.01171875, 0.0546875 * 1.00390625]:        # exact ties at m / 7
+        ms.append(float(nm.f32(np.array([7.0 * v]))[0]))
+    got = nm.bf16_rn(np.array(ms) / 7.0)
+    for m, g in zip(ms, got):
+        assert Fraction(g) == _bf16_rne_exact(Fraction(m) / 7), m
+
+
+def test_bf16s_codes_and_closed_form():
+    """Codes are the exact-rational RNE of w / sigma clamped to [-8, 7]; a group whose maximum
+    is 7 x (a bf16 value) gets exactly that sigma and code 7 there; a zero group gets sigma 0."""
+    rng = np.random.default_rng(2502)
+    W = nm.bf16_rn(rng.standard_normal((128, 384)) * 0.05)
+    W[3, 0] = 7 * 0.25                                  # group (3, 0): sigma = 0.25 exactly
+    W[3, 1:128] = np.clip(W[3, 1:128], -1.75, 1.75)
+    W[5, 128:256] = 0.0
+    q = quant.quantize_weight_bf16s(W, 0)
+    Wt = W * 2.0 ** q.n
+    assert q.sigma[3, 0] == 0.25 * 2.0 ** q.n and q.codes[3, 0] == 7
+    assert q.sigma[5, 1] == 0 and not q.codes[5, 128:256].any()
+    for (r, g) in [(0, 0), (3, 0), (77, 2), (127, 1)]:
+        sig = Fraction(q.sigma[r, g])
+        for k in range(g * 128, g * 128 + 128, 7):
+            x = Fraction(Wt[r, k]) / sig
+            fl = x.numerator // x.denominator
+            rem = x - fl
+            rne = fl + (1 if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and fl % 2 == 1) else 0)
+            assert q.codes[r, k] == max(-8, min(7, rne))
+    # packing: same codes layout as layout v1; scales blocked like the FP8 scale codes
+    assert np.array_equal(layout.unpack_codes(q.packed, 128, 384), q.codes)
+    assert np.array_equal(q.scales16[layout.scale_index(np.full(3, 3), np.arange(3), 384)], q.sigma_bits[3])
+
+
+def test_bf16s_reference_vs_fraction():
+    """gemm_reference_bf16s against an exact-rational sum on a tiny problem."""
+    rng = np.random.default_rng(2503)
+    W = nm.bf16_rn(rng.standard_normal((128, 256)) * 0.03)
+    X = nm.bf16_rn(rng.standard_normal((2, 256)))
+    q = quant.quantize_weight_bf16s(W, 1)
+    xq, beta = quant.quantize_act(X, q.c)
+    r = gemm.gemm_reference_bf16s(xq, beta, q.codes, q.sigma, q.n)
+    xv = nm.E4M3_DECODE[xq]
+    for m in range(2):
+        for n in (0, 5, 127):
+            s = sum(Fraction(xv[m, k]) * int(q.codes[n, k]) * Fraction(q.sigma[n, k // 128]) for k in range(256))
+            exact = s * Fraction(beta[m]) / (Fraction(2) ** q.n)
+            assert abs(float(exact) - r[m, n]) <= 1e-12 * max(1.0, abs(float(exact)))
