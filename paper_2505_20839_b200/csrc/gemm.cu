@@ -68,7 +68,9 @@ struct GemmArgs {
     unsigned U;            // stream-K units = R * G (< 2^31: R < 2 * SMs, G <= K / 128)
     unsigned Cs;           // CTAs sharing the U units: min(C, U), so every sharer has >= 1 unit
                            // (a contributor with an empty range would never publish its partial)
-    int S;                 // > 1: cluster split-K, one tile per cluster of S CTAs (K split S ways)
+    int S;                 // > 1: split-K, S CTAs per tile (K split S ways): cluster split-K (rs = 0)
+                           // or L2 reduce-scatter split-K (rs = 1)
+    int rs;                // 1: rank q of a tile's S CTAs reduces the token chunks ch with ch % S == q
     int depth;             // weight stages in flight (<= STAGES): bounds the loaded HBM latency
     // out_layout 2 (SwiGLU pairs): tile rows [0, 64) are gate channels j0 + r, rows [64, 128)
     // the up channels of the same j; h = bf16(silu(g) * u) -> h_out[m][j], per-token
@@ -111,12 +113,15 @@ __device__ __forceinline__ long long prof_clock() {
 // second per-CTA timeline (epilogue): trace[C*16 + 512 + cta*16 + slot]
 #define FIREQ_TRACE2(slot) do { if (a.trace && (slot) < 16) \
     a.trace[a.C * 16 + 512 + blockIdx.x * 16 + (slot)] = gtimer(); } while (0)
+#define FIREQ_TRACE2_VAL(slot, v) do { if (a.trace && (slot) < 16) \
+    a.trace[a.C * 16 + 512 + blockIdx.x * 16 + (slot)] = (v); } while (0)
 #else
 #define FIREQ_TRACE(slot) do { } while (0)
 #define FIREQ_TRACE_VAL(slot, v) do { } while (0)
 #define FIREQ_TRACE_X(slot) do { } while (0)
 #define FIREQ_EVT(stage, ev) do { } while (0)
 #define FIREQ_TRACE2(slot) do { } while (0)
+#define FIREQ_TRACE2_VAL(slot, v) do { } while (0)
 #endif
 
 // First stream-K unit of CTA c: the U units are split contiguously over the first Cs CTAs.
@@ -198,6 +203,20 @@ __device__ __forceinline__ int owner_of(unsigned u, unsigned U, int C) {
 }
 
 
+// rs split-K (S ranks): 8 KB blocks a rank holds in its rings during the exchange -- incoming
+// (S - 1) * ceil(NT / S), outgoing NT - floor(NT / S) -- and the largest such count over the
+// S that make_plan may choose (it caps the total at kRsBudget bytes).
+constexpr int kRsBudget = 160 * 1024;
+__host__ __device__ constexpr int rs_blocks(int NT, int S) { return (S - 1) * ((NT + S - 1) / S) + NT - NT / S; }
+__host__ __device__ constexpr int rs_max_bytes(int NT) {
+    int m = 0;
+    for (int S = 2; S <= 8; ++S) {
+        const int b = rs_blocks(NT, S) * 8192;
+        if (b <= kRsBudget && b > m) m = b;
+    }
+    return m;
+}
+
 template <int NTOK, bool SIGN_SPLIT, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS, int NMMA>
 struct Cfg {
     static constexpr int kXBytes = NTOK * kGroup;                       // FP8 activation tile (1 group)
@@ -232,10 +251,11 @@ struct Cfg {
     // per-token scales, double-buffered by segment parity (2 x 256 floats) + 4 KB transpose
     static constexpr int kOffEpi = kOffFix + kFixSlots * kPartBytes;
     static constexpr int kOffBar = kOffEpi + 2048 + 16 * kTileN * 2;
-    static constexpr int kNumBars = 3 * STAGES + 2 * ASTAGES + 2 * ACCBUF + 2;
+    static constexpr int kNumBars = 3 * STAGES + 2 * ASTAGES + 2 * ACCBUF + 3;
     static constexpr int kOffMisc = kOffBar + kNumBars * 8;
     static constexpr int kSmemBytes = kOffMisc + 64 + 1024;             // + alignment slack
     static_assert(kXBytes % 1024 == 0, "X tile must keep 1024-B alignment");
+    static_assert(NTOK < 64 || kOffS - kOffX >= rs_max_bytes(NTOK / 16), "rs split-K blocks must fit the rings");
 };
 
 // Walks a CTA's units in pipeline stages of up to GPS consecutive groups of one tile
@@ -310,6 +330,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
     uint64_t* accempty = accfull + ACCBUF;
     uint64_t* fixbar = accempty + ACCBUF;
     uint64_t* ph1bar = fixbar + 1;          // NPH = 2: h quantized grid-wide (epilogue -> X producer)
+    uint64_t* rdybar = ph1bar + 1;          // rs split-K: the S - 1 peers' rings are free
     float* sFix = reinterpret_cast<float*>(smem + C::kOffFix);
     uint32_t* misc = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);   // [0] tmem base, [1] fixup flag
 
@@ -339,6 +360,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         for (int i = 0; i < ACCBUF; ++i) { ptx::mbar_init(&accfull[i], NMMA); ptx::mbar_init(&accempty[i], 4); }
         ptx::mbar_init(fixbar, 1);
         ptx::mbar_init(ph1bar, 1);
+        ptx::mbar_init(rdybar, a.S > 1 ? a.S - 1 : 1);
         ptx::fence_mbar_init();
         ptx::prefetch_tmap(&tmap_x0);
         if (NPH == 2) ptx::prefetch_tmap(&tmap_x1);
@@ -742,7 +764,8 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             sScale = sScaleBuf + (sg & 1) * 256;
             for (int t = r; t < NTOK; t += 128)
                 sScale[t] = (m0 + t < a.M) ? __fmul_rn(__bfloat162float(a.x_scale[m0 + t]), p2) : 0.0f;
-            const bool csplit = a.S > 1;
+            const bool csplit = a.S > 1 && !a.rs;
+            const bool rsplit = a.S > 1 && a.rs;
             const bool whole = (g0 == 0 && g1 == a.G) || csplit;
             // cluster split-K: rank 0 sums the ranks' partials in rank order; the other ranks
             // push theirs into rank 0's sFix slot q - 1 ([r][NTOK] fp32, 16-B units XOR-swizzled)
@@ -785,6 +808,100 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                 if (r == 0) FIREQ_TRACE2(12);
             }
             ptx::named_bar_sync(1, 128);            // sScale visible
+            if (NTOK >= 64 && rsplit) {
+                // Split-K reduce-scatter over the S CTAs (one cluster) of this tile: rank q owns
+                // the token chunks ch % S == q.  Once every rank's mainloop is done (its rings are
+                // idle: a single segment per CTA), each rank pushes its partial of every chunk it
+                // does not own into the owner's ring through DSMEM (st.async, transaction bytes on
+                // the owner's fixbar); the owner sums its chunks over the ranks in rank order
+                // (p_0 + p_1 + ...; its own partial from TMEM) and emits them.  All S ranks reduce
+                // at once; no global-memory round trip (through L2 the exchange of 6 MB of
+                // partials took ~6 us at M = 128, N = 4096).
+                const int q = (int)(blockIdx.x % a.S), S = a.S;
+                constexpr int NT = NTOK / 16;                     // token chunks per tile
+                const int nch = (NT - q + S - 1) / S;             // chunks this rank owns
+                const int nmax = (NT + S - 1) / S;
+                // rings: incoming blocks [0, (S - 1) * nmax), then this rank's outgoing blocks;
+                // a block is one chunk [16 tokens][128 rows] fp32 (8 KB).  S is capped so that
+                // (S - 1) * nmax + NT - NT / S blocks fit (make_plan).
+                float* fixbuf = reinterpret_cast<float*>(smem + C::kOffX);
+                float* outbuf = fixbuf + (S - 1) * nmax * 16 * kTileN;
+                constexpr int kBlk = 16 * kTileN;                 // floats per block
+                const uint32_t acc_t = tmem + lane_base + (uint32_t)(b * NMMA * NTOK);
+                if (r == 0) ptx::mbar_arrive_expect_tx(fixbar, (uint32_t)((S - 1) * nch * kBlk * 4));
+                // this rank's rings are free: tell every peer (remote arrive on its rdybar)
+                if (r < S && r != q) {
+                    const uint32_t rb = ptx::mapa_shared(ptx::smem_u32(rdybar), (uint32_t)r);
+                    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
+                }
+                // stage the chunks the peers own (TMEM -> own ring; conflict-free 4-B stores)
+                {
+                    int o = 0;
+#pragma unroll 1
+                    for (int ch = 0; ch < NT; ++ch) {
+                        if (ch % S == q) continue;
+                        uint32_t v[16];
+                        ptx::tmem_ld_x16(acc_t + ch * 16, v);
+                        ptx::tmem_wait_ld();
+                        float* dst = outbuf + o * kBlk + r;
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) dst[c * kTileN] = __uint_as_float(v[c]);
+                        ++o;
+                    }
+                }
+                ptx::fence_proxy_async_smem();          // staged stores visible to the bulk copies
+                ptx::named_bar_sync(1, 128);
+                if (r == 0) FIREQ_TRACE2(12);
+                ptx::mbar_wait(rdybar, 0);              // every peer's rings are free
+                if (r == 0) FIREQ_TRACE2(13);
+                if (r < 32) {
+                    if (ptx::elect_one()) {
+                        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+                        int o = 0;
+                        for (int ch = 0; ch < NT; ++ch) {
+                            const int p = ch % S;
+                            if (p == q) continue;
+                            const int k = (q < p ? q : q - 1) * ((NT - p + S - 1) / S) + ch / S;
+                            ptx::bulk_s2cluster(ptx::mapa_shared(ptx::smem_u32(fixbuf + k * kBlk), (uint32_t)p),
+                                                outbuf + o * kBlk, kBlk * 4,
+                                                ptx::mapa_shared(ptx::smem_u32(fixbar), (uint32_t)p));
+                            ++o;
+                        }
+                    }
+                    __syncwarp();
+                }
+                ptx::mbar_wait(fixbar, fix_phase);
+                fix_phase ^= 1u;
+                if (r == 0 && sg < 4) FIREQ_TRACE2(3 * sg + 1);
+#pragma unroll 1
+                for (int e = 0; e < nch; ++e) {
+                    const int ch = q + e * S;
+                    uint32_t v[16];
+                    ptx::tmem_ld_x16(acc_t + ch * 16, v);
+                    ptx::tmem_wait_ld();
+                    float accv[16];
+                    for (int qq = 0; qq < S; ++qq) {
+                        if (qq == q) {
+#pragma unroll
+                            for (int c = 0; c < 16; ++c)
+                                accv[c] = qq == 0 ? __uint_as_float(v[c]) : __fadd_rn(accv[c], __uint_as_float(v[c]));
+                        } else {
+                            const float* src = fixbuf + ((qq < q ? qq : qq - 1) * nch + e) * kBlk + r;
+#pragma unroll
+                            for (int c = 0; c < 16; ++c)
+                                accv[c] = qq == 0 ? src[c * kTileN] : __fadd_rn(accv[c], src[c * kTileN]);
+                        }
+                    }
+                    emit(accv, ch);
+                    if (r == 0 && e == 0) FIREQ_TRACE2(14);
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&accempty[b]);
+                if (r == 0 && sg < 4) FIREQ_TRACE2(3 * sg + 2);
+                ++sg;
+                continue;
+            }
             constexpr int kChUnroll = NTOK <= 32 ? NTOK / 16 : 1;   // static indices into own[]
 #pragma unroll kChUnroll
             for (int ch = 0; ch < (big_own ? 0 : NTOK / 16); ++ch) {
@@ -929,6 +1046,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                         __syncwarp();
                         ptx::mbar_wait(fixbar, fix_phase);
                         fix_phase ^= 1u;
+                        if (r == 0) { if (cc0 == c_lo + 1) FIREQ_TRACE2(13); else FIREQ_TRACE2(15); }
 #pragma unroll 1
                         for (int ch = 0; ch < NTOK / 16; ++ch) {
                             // running sum in CTA order: own (TMEM) + c_lo+1 + ... + c_hi
@@ -955,6 +1073,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                         }
                         if (!final) ptx::tmem_wait_st();
                         ptx::named_bar_sync(1, 128);      // fixbuf reuse
+                        if (r == 0 && cc0 == c_lo + 1) FIREQ_TRACE2(14);
                     }
                 } else if (misc[1]) {
                     __threadfence();
@@ -1097,6 +1216,9 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
+    // rs split-K: a rank's outgoing bulk copies read its SMEM until the peers have received
+    // them (completion is signalled only on the receivers' barriers): leave together
+    if (a.S > 1 && a.rs) ptx::cluster_sync();
     if (warp == kWAlloc) ptx::tmem_dealloc(tmem, C::kTmemCols);
     if (threadIdx.x == 0) FIREQ_TRACE(5);
     span_end(a.span);
@@ -1173,6 +1295,7 @@ namespace {
 
 struct Plan {
     int ntok, m_tiles, n_tiles, tiles, G, mode, C, R, S;
+    int rs;                // S-way split-K reduced through L2 (reduce-scatter), mode 3
     int Cs;                // CTAs sharing the stream-K units
     long long U;
     bool sign_split;
@@ -1185,7 +1308,7 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, bool allow_cluster = true) {
     // its coarser m-tile padding costs > 5% more MMA work than 192-token tiles
     p.ntok = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 192;
     if (M > 128 && 224 * ((M + 223) / 224) * 100 <= 105 * 192 * ((M + 191) / 192)) p.ntok = 224;
-    p.sign_split = p.ntok <= 128;
+    p.sign_split = p.ntok <= 64;
     p.m_tiles = (int)((M + p.ntok - 1) / p.ntok);
     p.n_tiles = (int)(N / kTileN);
     p.tiles = p.m_tiles * p.n_tiles;
@@ -1222,6 +1345,26 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, bool allow_cluster = true) {
         if (S > 1) {
             p.S = S;
             p.mode = 2;
+            p.R = 0;
+            p.U = 0;
+            p.Cs = 0;
+            p.C = p.tiles * S;
+        }
+    }
+    // Few tiles of >= 64 tokens: S-way split-K over a cluster whose S CTAs reduce the tile
+    // together through DSMEM, each its 1/S of the token chunks, received into its idle rings
+    // (a stream-K owner pulling S - 1 partials of 32-64 KB alone took ~10 us at M = 128,
+    // N = 4096; the same reduce-scatter through L2 ~6 us).
+    static const bool no_rsplit = getenv("FIREQ_NO_RSPLIT") != nullptr;
+    if (allow_cluster && !no_rsplit && p.S == 1 && p.ntok >= 64 && 2 * p.tiles <= sms) {
+        int S = std::min(std::min(sms / p.tiles, 8), p.G);
+        // the exchange's 8 KB blocks must fit the idle X + W rings (Cfg asserts rs_max_bytes)
+        const int NT = p.ntok / 16;
+        while (S > 1 && rs_blocks(NT, S) * 8192 > kRsBudget) --S;
+        if (S > 1) {
+            p.S = S;
+            p.rs = 1;
+            p.mode = 3;
             p.R = 0;
             p.U = 0;
             p.Cs = 0;
@@ -1312,6 +1455,7 @@ GemmArgs base_args(const Plan& p, int64_t M, int64_t N, int64_t K, const uint8_t
     args.U = (unsigned)p.U;
     args.Cs = (unsigned)p.Cs;
     args.S = p.S;
+    args.rs = p.rs;
     {
 #if FIREQ_PROFILE
         static const int depth = getenv("FIREQ_DEPTH") ? atoi(getenv("FIREQ_DEPTH")) : 1000;   // experiments
@@ -1372,8 +1516,10 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
         //  group per stage with 7 TMEM A stages, 2 converter warpgroups -- all slower)
         case 16:  return launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map, args, stream);
         case 32:  return launch_cfg<32, true, 3, 7, 3, 2, 2, 1>(map, args, stream);
+        // 64 tokens: sign-split (mask-select measured 3% slower); 128 tokens: mask-select (half
+        // the MMAs of N = 128; sign-split measured 6-12% slower at M = 128, N = 4096 / 14336)
         case 64:  return launch_cfg<64, true, 2, 5, 2, 2, 2, 1>(map, args, stream);
-        case 128: return launch_cfg<128, true, 2, 7, 4, 2, 1, 1>(map, args, stream);
+        case 128: return launch_cfg<128, false, 2, 8, 4, 2, 1, 1>(map, args, stream);
         case 224: return launch_cfg<224, false, 2, 5, 2, 2, 1, 1>(map, args, stream);   // TMEM 448 + 64
         default:  return launch_cfg<192, false, 2, 6, 4, 2, 1, 1>(map, args, stream);
     }

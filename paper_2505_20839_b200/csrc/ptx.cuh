@@ -89,6 +89,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32
         ::"r"(smem_u32(dst_smem)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
+// Bulk copy from this CTA's shared memory into CTA-cluster peer shared memory (dst, mbar:
+// mapa'd addresses); completes transaction bytes on the peer's mbarrier.
+__device__ __forceinline__ void bulk_s2cluster(uint32_t dst_cluster, const void* src_smem, uint32_t bytes,
+                                               uint32_t mbar_cluster) {
+    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst_cluster), "r"(smem_u32(src_smem)), "r"(bytes), "r"(mbar_cluster) : "memory");
+}
 // 16-byte asynchronous global -> shared copy (LDGSTS; L2 only), zero-filled when src_bytes = 0.
 __device__ __forceinline__ void cp_async_16(void* dst_smem, const void* src, uint32_t src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"

@@ -8,7 +8,7 @@ from paper_2505_20839_b200 import fireq as F
 F.load()
 R = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 cases = [(16, 22016, 4096), (16, 4096, 11008), (16, 1024, 4096), (16, 150 * 128, 512), (32, 4096, 14336),
-         (64, 4096, 14336), (128, 4096, 14336), (300, 9600, 512), (1024, 4096, 14336), (4096, 1024, 4096),
+         (64, 4096, 14336), (128, 4096, 14336), (256, 4096, 14336), (100, 256, 768), (300, 256, 384), (300, 9600, 512), (1024, 4096, 14336), (4096, 1024, 4096),
          (16384, 4096, 4096)]
 bad = 0
 for M, N, K in cases:

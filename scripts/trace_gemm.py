@@ -65,4 +65,9 @@ for (M, N, K) in SHAPES:
         rel2 = np.where(t2 > 0, (t2 - t0) / 1000.0, np.nan)
         print("   epilogue per segment: accfull seen / arrived (stream-K) / segment done")
         for c in order[:12]:
-            print(f"   {c:4d} " + " ".join(f"{v:7.2f}" for v in rel2[c, :12]))
+            print(f"   {c:4d} " + " ".join(f"{v:7.2f}" for v in rel2[c, :16]))
+        if os.environ.get("RAW_COLS"):
+            cols = [int(v) for v in os.environ["RAW_COLS"].split(",")]
+            print("   raw values (cycles) of trace2 cols", cols)
+            for c in order[:12]:
+                print(f"   {c:4d} " + " ".join(f"{t2[c, j]:10d}" for j in cols))
