@@ -69,7 +69,7 @@ struct GemmArgs {
     unsigned Cs;           // CTAs sharing the U units: min(C, U), so every sharer has >= 1 unit
                            // (a contributor with an empty range would never publish its partial)
     int S;                 // > 1: split-K, S CTAs per tile (K split S ways): cluster split-K (rs = 0)
-                           // or L2 reduce-scatter split-K (rs = 1)
+                           // or cluster split-K with a DSMEM reduce-scatter (rs = 1)
     int rs;                // 1: rank q of a tile's S CTAs reduces the token chunks ch with ch % S == q
     int depth;             // weight stages in flight (<= STAGES): bounds the loaded HBM latency
     // out_layout 2 (SwiGLU pairs): tile rows [0, 64) are gate channels j0 + r, rows [64, 128)
@@ -1295,7 +1295,7 @@ namespace {
 
 struct Plan {
     int ntok, m_tiles, n_tiles, tiles, G, mode, C, R, S;
-    int rs;                // S-way split-K reduced through L2 (reduce-scatter), mode 3
+    int rs;                // cluster split-K reduced by all S ranks (DSMEM reduce-scatter), mode 3
     int Cs;                // CTAs sharing the stream-K units
     long long U;
     bool sign_split;

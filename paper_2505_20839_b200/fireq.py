@@ -149,7 +149,7 @@ def layout_version():
 def gemm_plan(M, N, K):
     cfg = (ctypes.c_int32 * 4)()
     _check(lib().fireq_gemm_plan(M, N, K, ctypes.cast(cfg, ctypes.c_void_p)), "fireq_gemm_plan")
-    return {"ntok": cfg[0], "mode": ("tiles", "stream-k", "cluster-split-k", "split-k-l2")[cfg[1]], "ctas": cfg[2], "sign_split": bool(cfg[3])}
+    return {"ntok": cfg[0], "mode": ("tiles", "stream-k", "cluster-split-k", "split-k-dsmem")[cfg[1]], "ctas": cfg[2], "sign_split": bool(cfg[3])}
 
 
 # ------------------------------------------------------------------- calls
