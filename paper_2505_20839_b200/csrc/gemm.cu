@@ -513,14 +513,17 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         bool touched = false;
         bool a_ready = false;    // afull of stage i already seen complete by the previous stage's probe
         bool p1_seen = false;
-        long long w_afull = 0, w_full = 0, t_issue = 0, t_mma0 = prof_clock();
+        long long w_afull = 0, w_full = 0, t_issue = 0, w_acc = 0, w_fence = 0, w_iter = 0, t_mma0 = prof_clock();
         for (int ph = 0; ph < NPH; ++ph) {
         const GemmArgs& a = ph ? a1 : a0;
         st.init(a, blockIdx.x);
         while (st.next(nt, mt, g, ng, sfirst, slast)) {
+            const long long c_it = prof_clock();
             const int b = sg % ACCBUF;
             if (sfirst) {
+                const long long ca = prof_clock();
                 ptx::mbar_wait(&accempty[b], ((sg / ACCBUF) & 1) ^ 1);
+                w_acc += prof_clock() - ca;
                 d = tmem + (b * NMMA + w) * NTOK;
                 touched = false;
             }
@@ -534,10 +537,12 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                 if (!C::kFoldX) ptx::mbar_wait(&fullX[s], (i / STAGES) & 1);
                 if (lane == 0) FIREQ_EVT(i, 5);
                 w_afull += c1 - c0;
-                w_full += prof_clock() - c1;
+                const long long cf = prof_clock();
+                w_full += cf - c1;
                 ptx::tc_fence_after();
                 const uint32_t ta = tmem + C::kACol0 + as * C::kASz;
                 const long long c2 = prof_clock();
+                w_fence += c2 - cf;
                 // probe the next stage's A barrier now: its round trip overlaps this stage's MMA
                 // issue (a stale "not yet" falls back to the blocking wait; a phase of a stage
                 // that does not exist is never used)
@@ -575,6 +580,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                 ++sg;
             }
             ++i;
+            w_iter += prof_clock() - c_it;
         }
         }
         if (lane == 0 && w == 0 && !(a.dbg & 64)) {
@@ -583,6 +589,9 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             FIREQ_TRACE_VAL(10, w_full);
             FIREQ_TRACE_VAL(11, prof_clock() - t_mma0);
             FIREQ_TRACE_VAL(15, t_issue);
+            FIREQ_TRACE2_VAL(15, w_acc);
+            FIREQ_TRACE2_VAL(13, w_fence);
+            FIREQ_TRACE2_VAL(14, w_iter);
         }
     } else if (warp < kWEpi) {
         // ------------------------------------------------------- converters
@@ -1518,8 +1527,10 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
         case 32:  return launch_cfg<32, true, 3, 7, 3, 2, 2, 1>(map, args, stream);
         // 64 tokens: sign-split (mask-select measured 3% slower); 128 tokens: mask-select (half
         // the MMAs of N = 128; sign-split measured 6-12% slower at M = 128, N = 4096 / 14336)
+        // with 2 groups per stage (3-6% faster than 1: half the MMA warp's per-stage work; no
+        // gain at 192 tokens)
         case 64:  return launch_cfg<64, true, 2, 5, 2, 2, 2, 1>(map, args, stream);
-        case 128: return launch_cfg<128, false, 2, 8, 4, 2, 1, 1>(map, args, stream);
+        case 128: return launch_cfg<128, false, 2, 4, 4, 2, 2, 1>(map, args, stream);
         case 224: return launch_cfg<224, false, 2, 5, 2, 2, 1, 1>(map, args, stream);   // TMEM 448 + 64
         default:  return launch_cfg<192, false, 2, 6, 4, 2, 1, 1>(map, args, stream);
     }

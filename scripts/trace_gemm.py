@@ -54,6 +54,11 @@ for (M, N, K) in SHAPES:
     cn = ["(first_W_issue)", "mma_wait_afull", "mma_wait_full", "mma_total", "conv_wait_full", "conv_wait_aempty", "conv_total", "mma_issue"]
     for j, nm in enumerate(cn):
         print(f"   cyc {nm:18s} med={np.median(cyc[:, j]):9.0f}")
+    t2all = tr.cpu().numpy()[plan["ctas"] * 16 + 512:].reshape(-1, 16).astype(np.int64)
+    if os.environ.get("ACC_WAIT") and plan["mode"] != "split-k-dsmem":
+        print(f"   cyc {'mma_wait_accempty':18s} med={np.median(t2all[:plan['ctas'], 15]):9.0f}")
+        print(f"   cyc {'mma_fence_after':18s} med={np.median(t2all[:plan['ctas'], 13]):9.0f}")
+        print(f"   cyc {'mma_iter_sum':18s} med={np.median(t2all[:plan['ctas'], 14]):9.0f}")
     del W, X, qw, rot
     torch.cuda.empty_cache()
     if os.environ.get("TRACE_SLOW"):
