@@ -465,13 +465,15 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         }
     } else if (warp == kWProdX) {
         // ------------------------------------------------------- activation producer
-        // decode: the activation tile is re-read by every n-tile; prefill: the concurrent CTAs
-        // share one m-tile, then it is dead
+        // the activation tile is re-read by every n-tile (decode) / by the concurrent CTAs of
+        // an m-tile (prefill): keep it in L2
         int i = 0;
         for (int ph = 0; ph < NPH; ++ph) {
         const GemmArgs& a = ph ? a1 : a0;
         const CUtensorMap& tmap_x = ph ? tmap_x1 : tmap_x0;
-        const uint64_t pol_x = a.m_tiles == 1 ? ptx::policy_evict_last() : ptx::policy_evict_first();
+        // (prefill: every concurrent CTA of an m-tile re-reads its X tiles as the CTAs drift
+        // apart; evict_first lost ~0.3 GB of them to DRAM re-reads per 16384 x 22016 launch)
+        const uint64_t pol_x = ptx::policy_evict_last();
         if (ph == 0) {
             ptx::pdl_wait();                // activations are written by the previous kernel
         } else {
@@ -747,9 +749,13 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
                     const int piece = r + 128 * k, row = piece >> 4, seg = piece & 15;
-                    if (mb + row < a.M)
-                        *reinterpret_cast<uint4*>(a.Y + (size_t)(mb + row) * a.ldy + ntile * kTileN + seg * 8) =
-                            *reinterpret_cast<const uint4*>(sT + row * kTileN + seg * 8);
+                    if (mb + row < a.M) {
+                        uint4* dst = reinterpret_cast<uint4*>(a.Y + (size_t)(mb + row) * a.ldy + ntile * kTileN + seg * 8);
+                        const uint4 val = *reinterpret_cast<const uint4*>(sT + row * kTileN + seg * 8);
+                        // prefill: Y is streamed out (evict-first stores) so that it does not push
+                        // the weights and X tiles out of L2; decode keeps Y for the next kernel
+                        if (a.m_tiles > 1) __stcs(dst, val); else *dst = val;
+                    }
                 }
                 ptx::named_bar_sync(1, 128);
             }
@@ -1479,6 +1485,7 @@ GemmArgs base_args(const Plan& p, int64_t M, int64_t N, int64_t K, const uint8_t
     args.pf_ptr[1] = static_cast<const uint8_t*>(pf1);
     args.pf_bytes[1] = pf1 ? (pf1_bytes & ~size_t(15)) : 0;
     args.span = next_span_slot();
+
 #if FIREQ_PROFILE
     {   // experiments only (profile builds): skip parts of the work
         static const int dbg = getenv("FIREQ_DEBUG_MODE") ? atoi(getenv("FIREQ_DEBUG_MODE")) : 0;
