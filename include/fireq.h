@@ -357,6 +357,10 @@ size_t fireq_ffn_workspace_bytes(int64_t M, int64_t d_model, int64_t d_ff);
  * FIREQ_ERROR_UNSUPPORTED_SHAPE.  Same arithmetic as the unfused chain
  * (quantize_act -> gemm -> silu_mul_quantize_act -> gemm) up to the fp32 summation
  * order of split tiles; y equals fireq_w4a8_gemm(quantize_act(h), W_down) exactly.
+ * Environment FIREQ_FFN_PERSISTENT=1 (read once per process): ONE persistent launch
+ * instead (x quantized in-kernel, three grid-wide barriers, the down phase scheduled
+ * stream-K: y then equals the standalone down GEMM under FIREQ_NO_CSPLIT=1 exactly);
+ * measured slower on B200, kept for the record.
  */
 fireq_status_t fireq_ffn_w4a8_decode(const void* x, int64_t ldx, const void* c_gu, int64_t M,
                                      int64_t d_model, int64_t d_ff, const uint8_t* gu_packed,

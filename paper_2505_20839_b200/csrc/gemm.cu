@@ -84,6 +84,14 @@ struct GemmArgs {
     uint8_t* hq_out;
     __nv_bfloat16* hbeta_out;
     unsigned* bar;
+    // single-launch FFN (NPH = 2, phase 0 only): the grid also quantizes its own input x
+    // (A1..A3 of fireq_quantize_act, CTA m < M takes token row m) into the X_hat buffer its
+    // tensor map points to (xq_out) and beta (x_scale), then passes a grid-wide barrier
+    // (bar[4] arrivals, bar[5] departures) before any activation tile is loaded
+    const __nv_bfloat16* x_in;   // bf16 [M][ldx_in], or nullptr (X_hat given)
+    int64_t ldx_in;
+    const __nv_bfloat16* x_chan; // c_k (nullable)
+    uint8_t* xq_out;
     unsigned long long* trace;   // debug timeline [C][8] (%globaltimer ns) or nullptr
     int dbg;                     // experiments only: bit0 skip conversion, bit1 skip MMAs, bit2 skip weight loads
     unsigned long long* span;    // profile builds: {start, end} of this launch
@@ -115,7 +123,10 @@ __device__ __forceinline__ long long prof_clock() {
     a.trace[a.C * 16 + 512 + blockIdx.x * 16 + (slot)] = gtimer(); } while (0)
 #define FIREQ_TRACE2_VAL(slot, v) do { if (a.trace && (slot) < 16) \
     a.trace[a.C * 16 + 512 + blockIdx.x * 16 + (slot)] = (v); } while (0)
+// third per-CTA timeline (phases of the single-launch FFN): trace[C*32 + 512 + cta*16 + slot]
+#define FIREQ_TRACE3(slot) do { if (a0.trace) a0.trace[a0.C * 32 + 512 + blockIdx.x * 16 + (slot)] = gtimer(); } while (0)
 #else
+#define FIREQ_TRACE3(slot) do { } while (0)
 #define FIREQ_TRACE(slot) do { } while (0)
 #define FIREQ_TRACE_VAL(slot, v) do { } while (0)
 #define FIREQ_TRACE_X(slot) do { } while (0)
@@ -251,7 +262,7 @@ struct Cfg {
     // per-token scales, double-buffered by segment parity (2 x 256 floats) + 4 KB transpose
     static constexpr int kOffEpi = kOffFix + kFixSlots * kPartBytes;
     static constexpr int kOffBar = kOffEpi + 2048 + 16 * kTileN * 2;
-    static constexpr int kNumBars = 3 * STAGES + 2 * ASTAGES + 2 * ACCBUF + 3;
+    static constexpr int kNumBars = 3 * STAGES + 2 * ASTAGES + 2 * ACCBUF + 4;
     static constexpr int kOffMisc = kOffBar + kNumBars * 8;
     static constexpr int kSmemBytes = kOffMisc + 64 + 1024;             // + alignment slack
     static_assert(kXBytes % 1024 == 0, "X tile must keep 1024-B alignment");
@@ -306,8 +317,14 @@ struct StageIter {
 // counters running on; the weight producer streams (and the converters convert) the down
 // weights while phase 0 drains.  Only the activation producer and the epilogue wait for
 // the grid-wide h barrier before phase 1.
+#ifndef FIREQ_CONV_ROLL
+#define FIREQ_CONV_ROLL 0
+#endif
+constexpr int kConvUnrollJ = FIREQ_CONV_ROLL >= 1 ? 1 : 4;
+constexpr int kConvUnrollQ = FIREQ_CONV_ROLL >= 2 ? 1 : 4;
+
 template <int NTOK, bool SIGN_SPLIT, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS, int NMMA, int NPH>
-__global__ void __maxnreg__((NTOK <= 32 ? 88 : NTOK <= 64 ? 96 : 128))
+__global__ void __maxnreg__((NTOK <= 32 ? (NPH == 2 ? 96 : 88) : NTOK <= 64 ? 96 : 128))
 k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__ GemmArgs a0,
             const __grid_constant__ CUtensorMap tmap_x1, const __grid_constant__ GemmArgs a1) {
     using C = Cfg<NTOK, SIGN_SPLIT, NCONV, STAGES, ASTAGES, ACCBUF, GPS, NMMA>;
@@ -331,6 +348,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
     uint64_t* fixbar = accempty + ACCBUF;
     uint64_t* ph1bar = fixbar + 1;          // NPH = 2: h quantized grid-wide (epilogue -> X producer)
     uint64_t* rdybar = ph1bar + 1;          // rs split-K: the S - 1 peers' rings are free
+    uint64_t* x0bar = rdybar + 1;           // in-kernel x quantization done grid-wide (epilogue -> X producer)
     float* sFix = reinterpret_cast<float*>(smem + C::kOffFix);
     uint32_t* misc = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);   // [0] tmem base, [1] fixup flag
 
@@ -361,6 +379,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         ptx::mbar_init(fixbar, 1);
         ptx::mbar_init(ph1bar, 1);
         ptx::mbar_init(rdybar, a.S > 1 ? a.S - 1 : 1);
+        ptx::mbar_init(x0bar, 1);
         ptx::fence_mbar_init();
         ptx::prefetch_tmap(&tmap_x0);
         if (NPH == 2) ptx::prefetch_tmap(&tmap_x1);
@@ -428,13 +447,17 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         // decode: weights are streamed once (evict first); prefill: every m-tile re-reads
         // them, so keep them in L2 (the 126 MB L2 holds the largest layer's weights)
         int i = 0;
+        bool p1first = true;
+        if (lane == 0) FIREQ_TRACE_X(11);
         for (int ph = 0; ph < NPH; ++ph) {
         const GemmArgs& a = ph ? a1 : a0;
         const uint64_t pol_w = a.m_tiles == 1 ? ptx::policy_evict_first() : ptx::policy_evict_last();
         st.init(a, blockIdx.x);
+        if (lane == 0 && i == 0) FIREQ_TRACE_X(14);
         while (st.next(nt, mt, g, ng, sfirst, slast)) {
             const int s = i % STAGES;
             ptx::mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+            if (lane == 0 && i == 0) FIREQ_TRACE_X(15);
             // Keep at most `depth` stages in flight: past the point where HBM is saturated,
             // more outstanding bytes only lengthen the queue every other global access of
             // this kernel (epilogue stores, fixup loads) waits in.  Completion of stage j
@@ -444,9 +467,11 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                 const int j = i - a.depth;
                 ptx::mbar_wait(&empty[j % STAGES], (j / STAGES) & 1);
             }
+            if (NPH == 2 && ph == 1 && lane == 0 && p1first) { p1first = false; FIREQ_TRACE3(10); }
             issue_w(a, i, pol_w);
             ++i;
         }
+        if (lane == 0) FIREQ_TRACE3(9 + 2 * ph);
         }
         const GemmArgs& a = NPH == 2 ? a1 : a0;
         // Once this CTA's own weight loads are issued, stream its share of the NEXT layer's
@@ -476,11 +501,19 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         const uint64_t pol_x = ptx::policy_evict_last();
         if (ph == 0) {
             ptx::pdl_wait();                // activations are written by the previous kernel
+            if (NPH == 2 && a.x_in) {
+                // X_hat is produced by this grid (epilogue phase A, every CTA's slice
+                // published before the grid barrier the epilogue released x0bar after)
+                ptx::mbar_wait(x0bar, 0);
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                if (lane == 0) FIREQ_TRACE3(3);
+            }
         } else {
             // phase 1 reads h_hat, written by every CTA's epilogue tail (generic stores): the
             // epilogue passed the grid barrier with gpu-scope acquire, then released ph1bar
             ptx::mbar_wait(ph1bar, 0);
             asm volatile("fence.proxy.async.global;" ::: "memory");
+            if (lane == 0) FIREQ_TRACE3(6);
         }
         st.init(a, blockIdx.x);
         while (st.next(nt, mt, g, ng, sfirst, slast)) {
@@ -534,7 +567,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                 const long long c0 = prof_clock();
                 if (!a_ready) ptx::mbar_wait(&afull[as], (i / ASTAGES) & 1);
                 if (lane == 0) FIREQ_EVT(i, 4);
-                if (NPH == 2 && ph == 1 && lane == 0 && !p1_seen) { p1_seen = true; FIREQ_TRACE2(14); }
+                if (NPH == 2 && ph == 1 && lane == 0 && !p1_seen) { p1_seen = true; FIREQ_TRACE3(7); }
                 const long long c1 = prof_clock();
                 if (!C::kFoldX) ptx::mbar_wait(&fullX[s], (i / STAGES) & 1);
                 if (lane == 0) FIREQ_EVT(i, 5);
@@ -631,13 +664,13 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             ptx::tc_fence_after();
             if (!(FIREQ_PROFILE && (a.dbg & 1))) {
                 const uint32_t ta = tmem + lane_base + C::kACol0 + as * C::kASz;
-#pragma unroll
+#pragma unroll kConvUnrollQ
                 for (int q = 0; q < GPS; ++q) {
                     const uint4 L = sLut[sS[s * C::kSStage + q * kTileN + r] & 0x7F];
                     const uint8_t* wrow = sW + s * C::kWStage + q * kWBytes + r * 16;
                     if (SIGN_SPLIT) {
                         const uint32_t N0 = L.z & 0x7F7F7F7Fu, N1 = L.w & 0x7F7F7F7Fu;
-#pragma unroll
+#pragma unroll kConvUnrollJ
                         for (int j = 0; j < 4; ++j) {
                             const uint4 wv = *reinterpret_cast<const uint4*>(wrow + j * 128 * 16);
                             uint32_t P[8], Q[8];
@@ -679,6 +712,107 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         ptx::pdl_wait();                    // beta, workspace and Y are shared with earlier kernels
         const int r = threadIdx.x & 127;
         const uint32_t lane_base = (uint32_t)(r & ~31) << 16;
+        if (r == 0) FIREQ_TRACE3(0);
+        if (NPH == 2 && a0.x_in) {
+            // ---- phase A (single-launch FFN): x -> (x_hat, beta), A1..A3 with exactly
+            // fireq_quantize_act's arithmetic; CTA m < M quantizes token row m, then every CTA passes a
+            // grid-wide barrier before its activation producer loads x_hat tiles.
+            float* red = reinterpret_cast<float*>(smem + C::kOffEpi);     // (scale buffers: unused yet)
+            if ((int)blockIdx.x < a0.M) {
+                const int m = blockIdx.x, nv = a0.K / 8;
+                const __nv_bfloat16* xr = a0.x_in + (size_t)m * a0.ldx_in;
+                // x' of vector v (A1: bf16(x * c_k), the product exact in fp32)
+                auto xprime = [&](int v) {
+                    uint4 raw = __ldcg(reinterpret_cast<const uint4*>(xr) + v);
+                    if (a0.x_chan) {
+                        __nv_bfloat16* hx = reinterpret_cast<__nv_bfloat16*>(&raw);
+                        const uint4 rc = __ldg(reinterpret_cast<const uint4*>(a0.x_chan) + v);
+                        const __nv_bfloat16* hc = reinterpret_cast<const __nv_bfloat16*>(&rc);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)
+                            hx[i] = __float2bfloat16_rn(__fmul_rn(__bfloat162float(hx[i]), __bfloat162float(hc[i])));
+                    }
+                    return raw;
+                };
+                // vectors r, r + 128, ...: the first 4 stay in registers (K <= 4096; their loads
+                // all in flight at once), later ones are re-read for the encode pass
+                uint4 xv[4];
+                float amax = 0.0f;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (j * 128 + r < nv) xv[j] = __ldcg(reinterpret_cast<const uint4*>(xr) + j * 128 + r);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int v = j * 128 + r;
+                    if (v < nv) {
+                        __nv_bfloat16* hx = reinterpret_cast<__nv_bfloat16*>(&xv[j]);
+                        if (a0.x_chan) {
+                            const uint4 rc = __ldg(reinterpret_cast<const uint4*>(a0.x_chan) + v);
+                            const __nv_bfloat16* hc = reinterpret_cast<const __nv_bfloat16*>(&rc);
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+                                hx[i] = __float2bfloat16_rn(__fmul_rn(__bfloat162float(hx[i]), __bfloat162float(hc[i])));
+                        }
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) amax = fmaxf(amax, fabsf(__bfloat162float(hx[i])));
+                    }
+                }
+                for (int j = 4; j * 128 < nv; ++j) {
+                    const int v = j * 128 + r;
+                    if (v < nv) {
+                        const uint4 raw = xprime(v);
+                        const __nv_bfloat16* hx = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) amax = fmaxf(amax, fabsf(__bfloat162float(hx[i])));
+                    }
+                }
+                for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+                if (lane == 0) red[r >> 5] = amax;
+                ptx::named_bar_sync(1, 128);
+                amax = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+                // A2: beta = bf16_RN(amax / 448), 1 for an all-zero row
+                const __nv_bfloat16 bh = amax > 0.0f ? __float2bfloat16_rn(__fdiv_rn(amax, 448.0f))
+                                                     : __float2bfloat16_rn(1.0f);
+                const float beta = __bfloat162float(bh), rcp = __frcp_rn(beta);
+                if (r == 0) const_cast<__nv_bfloat16*>(a0.x_scale)[m] = bh;
+                // A3: x_hat = E4M3_RN_satfinite(x' / beta)
+                auto encode = [&](const uint4& raw, int v) {
+                    const __nv_bfloat16* hx = reinterpret_cast<const __nv_bfloat16*>(&raw);
+                    float f[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) f[i] = div_for_e4m3(__bfloat162float(hx[i]), beta, rcp);
+                    uint2 o;
+                    o.x = e4m3x2_rn(f[0], f[1]) | (e4m3x2_rn(f[2], f[3]) << 16);
+                    o.y = e4m3x2_rn(f[4], f[5]) | (e4m3x2_rn(f[6], f[7]) << 16);
+                    *reinterpret_cast<uint2*>(a0.xq_out + (size_t)m * a0.K + (size_t)v * 8) = o;
+                };
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (j * 128 + r < nv) encode(xv[j], j * 128 + r);
+                for (int j = 4; j * 128 < nv; ++j)
+                    if (j * 128 + r < nv) encode(xprime(j * 128 + r), j * 128 + r);
+                asm volatile("fence.proxy.async.global;" ::: "memory");   // read by other CTAs' TMA
+            }
+            ptx::named_bar_sync(1, 128);            // this CTA's x_hat / beta stores issued
+            if (r == 0) FIREQ_TRACE3(1);
+            if (r == 0) {
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a0.bar + 4) : "memory");
+                unsigned seen = 0;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(a0.bar + 4) : "memory");
+                    if (seen < gridDim.x) __nanosleep(32);
+                } while (seen < gridDim.x);
+                ptx::mbar_arrive(x0bar);            // release this CTA's activation producer
+                FIREQ_TRACE3(2);
+                unsigned prev;
+                asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a0.bar + 5) : "memory");
+                if (prev == gridDim.x - 1) {        // everyone has passed: reset for the next launch
+                    a0.bar[4] = 0u;
+                    a0.bar[5] = 0u;
+                }
+            }
+            ptx::named_bar_sync(1, 128);            // beta visible to this CTA's epilogue threads
+        }
         // [2][256]: segment sg uses buffer sg & 1, so a warp that runs ahead into the next
         // segment never overwrites scales another warp of this one still reads (the Y^T emit
         // has no barrier between segments)
@@ -1131,7 +1265,98 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             if (r == 0 && sg < 4) FIREQ_TRACE2(3 * sg + 2);
             ++sg;
         }
-        if (a.out_layout == 2 && a.hq_out) {
+        if (a.out_layout == 2 && a.hq_out && NPH == 2 && ph == 0) {
+            // ---- single-launch FFN, phase C: quantize h (A2..A3) once every tile's h and amax
+            // are in (grid barrier), each CTA a 1/C slice (one L2 round trip), then a second grid
+            // barrier before the down phase loads h_hat tiles.  (Quantizing exactly the groups
+            // a CTA's down units read instead -- no second barrier -- repeats each group for all
+            // 32 tiles: measured 19 us.)  Meanwhile the weight producer has streamed the down
+            // weights into the ring and the converters have filled the TMEM A stages.
+            ptx::named_bar_sync(1, 128);            // this CTA's h stores / amax atomics issued
+            if (r == 0) {
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar) : "memory");
+                unsigned seen = 0;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(a.bar) : "memory");
+                    if (seen < gridDim.x) __nanosleep(32);
+                } while (seen < gridDim.x);
+                FIREQ_TRACE3(4);
+            }
+            ptx::named_bar_sync(1, 128);
+            float* sB = sScaleBuf + ((sg & 1) ^ 1) * 256;   // beta_m, rcp(beta_m) (the buffer no segment uses next)
+            if (r < NTOK) {
+                const float amax = r < a.M ? __uint_as_float(__ldcg(a.amax_out + r)) : 0.0f;
+                const __nv_bfloat16 bh = amax > 0.0f ? __float2bfloat16_rn(__fdiv_rn(amax, 448.0f))
+                                                     : __float2bfloat16_rn(1.0f);
+                sB[r] = __bfloat162float(bh);
+                sB[NTOK + r] = __frcp_rn(__bfloat162float(bh));
+                if (r < a.M) a.hbeta_out[r] = bh;   // every CTA writes the same value
+            }
+            ptx::named_bar_sync(1, 128);            // amax read by this CTA
+            if (r == 0) {
+                // the last CTA past the barrier resets it and amax for the next launch
+                unsigned prev;
+                asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a.bar + 1) : "memory");
+                if (prev == gridDim.x - 1) {
+                    for (int m = 0; m < a.M; ++m) a.amax_out[m] = 0u;
+                    a.bar[0] = 0u;
+                    a.bar[1] = 0u;
+                }
+            }
+            // this CTA's slice of h_hat: 8-channel vectors [v0, v1) of the M x d_ff/8 vectors, all
+            // loads in flight at once (one L2 round trip; at most kSliceV vectors per thread)
+            {
+                const int nvrow = (int)(a.ldh / 8), tot = nvrow * a.M;
+                const int per = (tot + (int)gridDim.x - 1) / (int)gridDim.x;
+                const int v0 = (int)blockIdx.x * per, v1 = min(tot, v0 + per);
+                constexpr int kSliceV = 4;
+                for (int base = v0; base < v1; base += kSliceV * 128) {
+                    uint4 hv[kSliceV];
+#pragma unroll
+                    for (int u = 0; u < kSliceV; ++u) {
+                        const int idx = base + u * 128 + r;
+                        if (idx < v1) hv[u] = __ldcg(reinterpret_cast<const uint4*>(a.h_out) + (size_t)(idx / nvrow) * (a.ldh / 8) + idx % nvrow);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kSliceV; ++u) {
+                        const int idx = base + u * 128 + r;
+                        if (idx < v1) {
+                            const int m = idx / nvrow, v = idx % nvrow;
+                            const __nv_bfloat16* hh = reinterpret_cast<const __nv_bfloat16*>(&hv[u]);
+                            const float beta = sB[m], rcp = sB[NTOK + m];
+                            float f[8];
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) f[e] = div_for_e4m3(__bfloat162float(hh[e]), beta, rcp);
+                            uint2 o;
+                            o.x = e4m3x2_rn(f[0], f[1]) | (e4m3x2_rn(f[2], f[3]) << 16);
+                            o.y = e4m3x2_rn(f[4], f[5]) | (e4m3x2_rn(f[6], f[7]) << 16);
+                            *reinterpret_cast<uint2*>(a.hq_out + (size_t)m * a.ldh + (size_t)v * 8) = o;
+                        }
+                    }
+                }
+            }
+            asm volatile("fence.proxy.async.global;" ::: "memory");   // read by other CTAs' TMA
+            ptx::named_bar_sync(1, 128);            // this CTA's h_hat slice written
+            if (r == 0) {
+                FIREQ_TRACE3(5);
+                // second grid barrier (bar[2] arrivals, bar[3] departures): every slice of h_hat
+                // is written before any CTA's phase-1 activation loads
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar + 2) : "memory");
+                unsigned seen = 0;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(a.bar + 2) : "memory");
+                    if (seen < gridDim.x) __nanosleep(32);
+                } while (seen < gridDim.x);
+                ptx::mbar_arrive(ph1bar);           // release to this CTA's activation producer
+                FIREQ_TRACE3(8);
+                unsigned prev;
+                asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a.bar + 3) : "memory");
+                if (prev == gridDim.x - 1) {
+                    a.bar[2] = 0u;
+                    a.bar[3] = 0u;
+                }
+            }
+        } else if (a.out_layout == 2 && a.hq_out) {
             // ---- SwiGLU tail: quantize h (A2..A3) once every tile's h and amax are in.
             // Grid-wide barrier: every CTA of this persistent grid is resident (one per SM,
             // launched before any dependent kernel can take an SM), so spinning is safe.
@@ -1197,30 +1422,6 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                     a.bar[0] = 0u;
                     a.bar[1] = 0u;
                 }
-            }
-            if (NPH == 2 && ph == 0) {
-                // second grid barrier: every CTA's slice of h_hat (and hbeta) is written before
-                // any CTA's phase-1 activation loads / epilogue scales read them
-                ptx::named_bar_sync(1, 128);        // this CTA's h_hat stores issued
-                __threadfence();
-                ptx::named_bar_sync(1, 128);
-                if (r == 0) {
-                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar + 2) : "memory");
-                    unsigned seen = 0;
-                    do {
-                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(a.bar + 2) : "memory");
-                        if (seen < gridDim.x) __nanosleep(64);
-                    } while (seen < gridDim.x);
-                    ptx::mbar_arrive(ph1bar);       // release to this CTA's activation producer
-                    FIREQ_TRACE2(13);
-                    unsigned prev;
-                    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a.bar + 3) : "memory");
-                    if (prev == gridDim.x - 1) {    // everyone has passed: reset for the next launch
-                        a.bar[2] = 0u;
-                        a.bar[3] = 0u;
-                    }
-                }
-                ptx::named_bar_sync(1, 128);
             }
         }
         }                                           // phases
@@ -1571,12 +1772,14 @@ fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_b
     if (!ffn_shape_supported(M, d_model, d_ff))
         return fail(FIREQ_ERROR_UNSUPPORTED_SHAPE, "fused FFN: decode batches (M <= 16) only");
     if (ws_bytes < ffn_workspace_bytes(M, d_model, d_ff)) return fail(FIREQ_ERROR_WORKSPACE, "FFN workspace too small");
-    // Default: three kernels (act quant; gate_up with the SwiGLU tail; down with its own
-    // best plan, cluster split-K at decode).  FIREQ_FFN_PERSISTENT=1 runs gate_up and down
-    // in ONE persistent grid (NPH = 2, stream-K for both phases) -- measured slower so far
-    // (DESIGN.md "Fused decode FFN").
-    static const bool persistent = getenv("FIREQ_FFN_PERSISTENT") != nullptr;
-    const Plan p1 = make_plan(M, 2 * d_ff, d_model, false), p2 = make_plan(M, d_model, d_ff, !persistent);
+    // Default: three kernels (act quant; gate_up with the SwiGLU tail; down with its own best
+    // plan, cluster split-K at decode).  FIREQ_FFN_PERSISTENT=1: ONE persistent launch (NPH = 2):
+    // x quantized in-kernel (phase A, grid barrier), gate_up with the SwiGLU epilogue, grid
+    // barrier, each CTA quantizing a 1/C slice of h, grid barrier, down (stream-K for both
+    // phases).  Measured slower (41.5 vs 35.2 us for the Llama2-7B FFN): each phase boundary
+    // is ~6 serialized global round trips of ~0.7 us under load (fused decode FFN).
+    static const bool split = getenv("FIREQ_FFN_PERSISTENT") == nullptr;
+    const Plan p1 = make_plan(M, 2 * d_ff, d_model, false), p2 = make_plan(M, d_model, d_ff, split);
     uint8_t* w = static_cast<uint8_t*>(ws);
     uint8_t* ws1 = w;
     uint8_t* ws2 = ws1 + align256(plan_workspace_bytes(p1));
@@ -1587,9 +1790,6 @@ fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_b
     __nv_bfloat16* xbeta = reinterpret_cast<__nv_bfloat16*>(xq + align256((size_t)M * d_model));
     uint8_t* hq = reinterpret_cast<uint8_t*>(xbeta) + 256;
     __nv_bfloat16* hbeta = reinterpret_cast<__nv_bfloat16*>(hq + align256((size_t)M * d_ff));
-    // A1..A3 of x (the FFN input comes from the previous layer)
-    fireq_status_t st = quantize_act_impl(x, nullptr, M, d_model, ldx, c_gu, c_gu ? 1 : 0, false, xq, xbeta, stream);
-    if (st != FIREQ_SUCCESS) return st;
     // phase 0: gate_up over interleaved [gate | up] tiles; SwiGLU epilogue; h quantized in its tail
     CUtensorMap map1, map2;
     if (!make_x_map(&map1, xq, M, d_model, p1.ntok) || !make_x_map(&map2, hq, M, d_ff, p2.ntok))
@@ -1615,8 +1815,16 @@ fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_b
     if (trace_which == 2) a1.trace = nullptr;
     if (trace_which == 1) a2.trace = nullptr;
 #endif
-    if (persistent && p1.C == p2.C)
+    if (!split && p1.C == p2.C) {
+        // one launch: x quantized in-kernel (phase A), gate_up + SwiGLU, h quantized per CTA, down
+        a1.x_in = x;
+        a1.ldx_in = ldx;
+        a1.x_chan = c_gu;
+        a1.xq_out = xq;
         return launch_cfg<16, true, 3, 8, 3, 2, 2, 1, 2>(map1, a1, stream, &map2, &a2);
+    }
+    fireq_status_t st = quantize_act_impl(x, nullptr, M, d_model, ldx, c_gu, c_gu ? 1 : 0, false, xq, xbeta, stream);
+    if (st != FIREQ_SUCCESS) return st;
     st = launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map1, a1, stream);
     if (st != FIREQ_SUCCESS) return st;
     return launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map2, a2, stream);

@@ -1,7 +1,7 @@
 import os, sys, torch
 sys.path.insert(0, os.getcwd())
 from paper_2505_20839_b200 import fireq as F
-F.load()
+F.load(os.environ["LIB"]) if os.environ.get("LIB") else F.load()
 import bench
 dev = torch.device("cuda", 0)
 for name, cls in [("chain4", bench.FFN), ("fused", bench.FusedFFN)]:

@@ -14,7 +14,7 @@ with torch.cuda.stream(s):
         ffn.step(r % 4, s)
 torch.cuda.synchronize()
 C = 148
-tr = torch.zeros(C * 32 + 512 + 64, dtype=torch.int64, device=dev)
+tr = torch.zeros(C * 48 + 512 + 64, dtype=torch.int64, device=dev)
 for it in range(9):
     F.debug_set_trace(tr if it == 8 else None)
     with torch.cuda.stream(s):
@@ -32,7 +32,14 @@ def col(a, j):
 for nm, a, j in [("start", t1, 0), ("setup", t1, 1), ("first_data", t1, 2), ("mma_done", t1, 3), ("epi_done", t1, 4),
                  ("end", t1, 5), ("seg0 accfull", t2, 0), ("seg0 done", t2, 2), ("seg1 accfull", t2, 3), ("seg1 done", t2, 5),
                  ("seg2 accfull", t2, 6), ("seg2 done", t2, 8), ("seg3 accfull", t2, 9),
-                 ("barrier1 passed", t2, 15), ("barrier2 passed", t2, 13), ("phase1 first MMA", t2, 14)]:
+                 ]:
     c = col(a, j)
     if c.size:
         print(f"  {nm:18s} min={c.min():7.2f} med={np.median(c):7.2f} max={c.max():7.2f}  n={c.size}")
+t3 = t[C * 32 + 512: C * 32 + 512 + C * 16].reshape(C, 16)
+for nm, j in [("epi after pdl_wait", 0), ("phase A done", 1), ("G1 passed", 2), ("X prod ph0 start", 3),
+              ("W prod ph0 last issue", 9), ("G2 passed", 4), ("phase C slice done", 5), ("G3 passed", 8), ("X prod ph1 start", 6),
+              ("MMA ph1 first stage", 7), ("W prod ph1 first issue", 10), ("W prod done", 11)]:
+    c = col(t3, j)
+    if c.size:
+        print(f"  {nm:22s} min={c.min():7.2f} med={np.median(c):7.2f} max={c.max():7.2f}  n={c.size}")

@@ -112,30 +112,63 @@ def test_interleave_gate_up_is_a_row_permutation(fireq):
     assert qil.n == qgu.n and torch.equal(qil.c, qgu.c)
 
 
-@pytest.mark.parametrize("M,d,dff", [(16, 1024, 2816), (5, 512, 384), (1, 256, 128), (11, 768, 1280)])
-def test_fused_ffn_matches_unfused_chain(fireq, M, d, dff):
-    """The fused FFN = quantize_act -> gate_up (SwiGLU epilogue, h quantized in its tail) ->
-    down.  Exact checks: y equals the standalone down GEMM on quantize_act(h) (the tail's
-    quantization is A2..A3 bit for bit), and repeated calls agree (workspace reset).
-    Against the unfused 4-kernel chain: same h codes up to the fp32 summation order of
-    split tiles (the two paths schedule gate_up differently)."""
-    *_, qgu, qil, qd, x = _ffn_case(fireq, M, d, dff, 71 + M)
+def _check_fused(fireq, M, d, dff, seed, reps=3):
+    """The fused FFN against its pieces.  Exact: y equals the standalone down GEMM on
+    quantize_act(h) (the in-kernel A2..A3 of h is bit for bit fireq_quantize_act's; the
+    caller's environment makes the standalone GEMM take the fused path's down plan), and
+    repeated calls agree (workspace reset).  Against the unfused 4-kernel chain: G4."""
+    *_, qgu, qil, qd, x = _ffn_case(fireq, M, d, dff, seed)
     hq, hb, y_ref = _unfused(fireq, x, qgu, qd, dff)
     ws = fireq.Workspace(fireq.ffn_workspace_bytes(M, d, dff))
     h = torch.empty((M, dff), dtype=torch.bfloat16, device=DEV)
-    y = fireq.ffn_w4a8_decode(x, qil, qd, h=h, workspace=ws)
+    ys = [fireq.ffn_w4a8_decode(x, qil, qd, h=h, workspace=ws) for _ in range(reps)]
     hq2, hb2 = fireq.quantize_act(h)
     y2 = fireq.w4a8_gemm(hq2, hb2, qd.packed, qd.scales, d, qd.n)
     torch.cuda.synchronize()
-    # same h_hat (the tail's A2..A3 is bit-exact) and, by default, the same down plan as the
-    # standalone GEMM: y equals fireq_w4a8_gemm(quantize_act(h), W_down) bit for bit (fireq.h)
-    assert torch.equal(y, y2)
+    assert all(torch.equal(v, ys[0]) for v in ys)
+    assert torch.equal(ys[0], y2), (ys[0].float() - y2.float()).abs().max().item()
+    # h of the interleaved gate_up vs the plain one: same up to the fp32 summation order of
+    # split tiles (the two paths schedule gate_up differently)
     assert torch.allclose(hb2.float(), hb.float(), rtol=2 ** -7, atol=0)
     assert (hq2 == hq).float().mean().item() > 0.995
-    yv, rv = y.float().cpu().numpy().astype(np.float64), y_ref.float().cpu().numpy().astype(np.float64)
-    assert og.g4_error(yv, rv) <= 1e-2
-    for _ in range(3):
-        assert torch.equal(fireq.ffn_w4a8_decode(x, qil, qd, h=h, workspace=ws), y)
+    yv, rv = ys[0].float().cpu().numpy().astype(np.float64), y_ref.float().cpu().numpy().astype(np.float64)
+    assert og.g4_error(yv, rv) <= 1e-2 and og.rel_frobenius(yv, rv) < 2e-3
+
+
+def _isolated(call, env):
+    """Run `call` (source using F = fireq, T = this module) in a fresh process with `env`
+    added: the library reads its FIREQ_* switches once per process."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+            "from paper_2505_20839_b200 import fireq as F; F.load()\n"
+            "import test_gpu_ffn as T\n%s\nprint('ok')\n") % (root, os.path.join(root, "tests"), call)
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+FUSED_CASES = [(16, 1024, 2816), (5, 512, 384), (1, 256, 128), (11, 768, 1280), (16, 4096, 11008)]
+
+
+@pytest.mark.parametrize("M,d,dff", FUSED_CASES)
+def test_fused_ffn_three_kernels(fireq, M, d, dff):
+    """Default fireq_ffn_w4a8_decode: quantize_act(x); gate_up with the SwiGLU tail; down with
+    the standalone GEMM's own plan (cluster split-K at decode) -- y equals it bit for bit.
+    (4096 x 11008: Llama2-7B, 8 back-to-back calls.)"""
+    _check_fused(fireq, M, d, dff, 71 + M, reps=8 if d == 4096 else 3)
+
+
+@pytest.mark.parametrize("M,d,dff", [(16, 1024, 2816), (5, 512, 384), (16, 4096, 11008)])
+def test_fused_ffn_single_launch(M, d, dff):
+    """FIREQ_FFN_PERSISTENT=1: ONE persistent launch (x quantized in-kernel behind a grid
+    barrier, gate_up + SwiGLU, grid barrier, h quantized in 1/C slices, grid barrier, down by
+    stream-K).  FIREQ_NO_CSPLIT=1 gives the standalone down GEMM the same stream-K plan, so y
+    must match it bit for bit.  (1024 x 2816: gate_up is pure stream-K, 44 tiles < 148 CTAs: a
+    tile owner whose split tile is its last phase-0 segment must not stage partials through
+    the weight ring, which already streams phase-1 weights.)"""
+    _isolated("T._check_fused(F, %d, %d, %d, %d, reps=%d)" % (M, d, dff, 171 + M, 8 if d == 4096 else 3),
+              {"FIREQ_NO_CSPLIT": "1", "FIREQ_FFN_PERSISTENT": "1"})
 
 
 def test_fused_ffn_vs_oracle(fireq):
@@ -149,49 +182,3 @@ def test_fused_ffn_vs_oracle(fireq):
     yv = y.float().cpu().numpy().astype(np.float64)
     assert og.g4_error(yv, r) <= 2e-2                        # same bound as the unfused chain
     assert og.rel_frobenius(yv, r) < 5e-3
-
-
-def test_fused_ffn_llama2_7b(fireq):
-    """Full Llama2-7B FFN at batch 16, repeated back to back without host syncs."""
-    M, d, dff = 16, 4096, 11008
-    *_, qgu, qil, qd, x = _ffn_case(fireq, M, d, dff, 91)
-    hq, hb, y_ref = _unfused(fireq, x, qgu, qd, dff)
-    ws = fireq.Workspace(fireq.ffn_workspace_bytes(M, d, dff))
-    h = torch.empty((M, dff), dtype=torch.bfloat16, device=DEV)
-    ys = [fireq.ffn_w4a8_decode(x, qil, qd, h=h, workspace=ws) for _ in range(8)]
-    hq2, hb2 = fireq.quantize_act(h)
-    y2 = fireq.w4a8_gemm(hq2, hb2, qd.packed, qd.scales, d, qd.n)
-    torch.cuda.synchronize()
-    assert all(torch.equal(v, ys[0]) for v in ys)
-    assert torch.equal(ys[0], y2)                   # the down step, bit for bit (fireq.h)
-    assert torch.allclose(hb2.float(), hb.float(), rtol=2 ** -7, atol=0)
-    assert (hq2 == hq).float().mean().item() > 0.995
-    yv, rv = ys[0].float().cpu().numpy().astype(np.float64), y_ref.float().cpu().numpy().astype(np.float64)
-    assert og.g4_error(yv, rv) <= 1e-2 and og.rel_frobenius(yv, rv) < 2e-3
-
-
-def test_fused_ffn_persistent_pure_stream_k(fireq):
-    """FIREQ_FFN_PERSISTENT=1 (gate_up and down in one grid) at a shape whose gate_up plan is
-    pure stream-K (44 tiles < 148 CTAs): a tile owner whose split tile is its last phase-0
-    segment must not stage partials through the weight ring, which already streams phase-1
-    weights.  Runs in a subprocess (the switch is read once per process)."""
-    import os, subprocess, sys
-    code = (
-        "import sys, numpy as np, torch; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
-        "from paper_2505_20839_b200 import fireq as F; F.load()\n"
-        "import test_gpu_ffn as T\n"
-        "M, d, dff = 16, 1024, 2816\n"
-        "*_, qgu, qil, qd, x = T._ffn_case(F, M, d, dff, 171)\n"
-        "hq, hb, y_ref = T._unfused(F, x, qgu, qd, dff)\n"
-        "ws = F.Workspace(F.ffn_workspace_bytes(M, d, dff))\n"
-        "ys = [F.ffn_w4a8_decode(x, qil, qd, workspace=ws) for _ in range(20)]\n"
-        "torch.cuda.synchronize()\n"
-        "assert all(torch.equal(v, ys[0]) for v in ys)\n"
-        "from oracle import gemm as og\n"
-        "yv, rv = ys[0].float().cpu().numpy().astype(np.float64), y_ref.float().cpu().numpy().astype(np.float64)\n"
-        "e = og.g4_error(yv, rv); assert e <= 1e-2, e\n"
-        "print('ok', e)\n") % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                              os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, FIREQ_FFN_PERSISTENT="1")
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=240)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
