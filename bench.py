@@ -184,11 +184,11 @@ class FFN:
 
 
 class FusedFFN:
-    """The same FFN through fireq_ffn_w4a8_decode: 3 kernels per step (quantize_act(x);
-    gate_up with the SwiGLU epilogue and h's quantization in its tail; down).  W_gu in
-    the interleaved row order."""
+    """The same FFN through fireq_ffn_w4a8_decode: 4 kernels per step (quantize_act(x);
+    gate_up with the SwiGLU epilogue; quantize_act(h); down [+ residual in its epilogue]).
+    W_gu in the interleaved row order."""
 
-    KERNELS_PER_STEP = 3
+    KERNELS_PER_STEP = 4
 
     def __init__(self, F, M, rotations, dev):
         from types import SimpleNamespace as NS
@@ -209,12 +209,12 @@ class FusedFFN:
         self.y = torch.empty((M, D_MODEL), dtype=torch.bfloat16, device=dev)
         self.ws = F.Workspace(F.ffn_workspace_bytes(M, D_MODEL, D_FF), dev)
 
-    def step(self, r, stream=None):
+    def step(self, r, stream=None, residual=False):
         q_gu, q_d = self.rot[r]
         nxt = self.rot[(r + 1) % len(self.rot)][0]
         pf = (nxt.packed, nxt.scales) if os.environ.get("BENCH_PREFETCH", "1") == "1" else None
         self.F.ffn_w4a8_decode(self.x, q_gu, q_d, h=self.h, out=self.y, workspace=self.ws, stream=stream,
-                               prefetch=pf)
+                               prefetch=pf, residual=self.x if residual else None)
 
     def bytes_per_step(self):
         M = self.M
@@ -466,12 +466,13 @@ def run_fireq(args, rank, world, dev):
         F.w4a8_gemm(ffn.hq, ffn.hbeta, p_d, s_d, D_MODEL, ffn.n_d, out=ffn.y, workspace=ffn.ws2, stream=stream)
 
     # one launch per weight copy, copies in rotation (4 x 46.6 MB > L2): every launch streams
-    # its weights from HBM
-    reps = 100
-    g_gu = capture(lambda: [gu_only(r) for r in range(ROTATIONS)], stream)
-    ms_gu = time_graphs([g_gu], reps, 4, stream) / (reps * ROTATIONS)
-    g_d = capture(lambda: [d_only(r) for r in range(ROTATIONS)], stream)
-    ms_d = time_graphs([g_d], reps, 4, stream) / (reps * ROTATIONS)
+    # its weights from HBM; 32 PDL-chained launches per graph, so graph-replay gaps do not
+    # count as kernel time
+    reps, per_graph = 25, 8
+    g_gu = capture(lambda: [gu_only(r) for _ in range(per_graph) for r in range(ROTATIONS)], stream)
+    ms_gu = time_graphs([g_gu], reps, 2, stream) / (reps * ROTATIONS * per_graph)
+    g_d = capture(lambda: [d_only(r) for _ in range(per_graph) for r in range(ROTATIONS)], stream)
+    ms_d = time_graphs([g_d], reps, 2, stream) / (reps * ROTATIONS * per_graph)
     b_gu = gemm_bytes(M_DECODE, 2 * D_FF, D_MODEL)
     gbs_gu = b_gu / (ms_gu * 1e-3) / 1e9
     b_d = gemm_bytes(M_DECODE, D_MODEL, D_FF)
@@ -486,6 +487,19 @@ def run_fireq(args, rank, world, dev):
     gf_multi = capture(lambda: [fused.step(r, stream) for r in range(ROTATIONS)], stream)
     gf_single = [capture(lambda r=r: fused.step(r, stream), stream) for r in range(ROTATIONS)]
     fused_us = time_steps(gf_multi, gf_single, args.steps, args.warmup, stream) * 1e3 / args.steps
+    del gf_multi, gf_single
+    # the unfused FFN block: the 4-kernel chain + the residual add as its own kernel
+    def chain_res(r):
+        ffn.step(r, stream)
+        ffn.y.add_(ffn.x)
+    g_cr = capture(lambda: [chain_res(r) for r in range(ROTATIONS)], stream)
+    g_cr1 = [capture(lambda r=r: chain_res(r), stream) for r in range(ROTATIONS)]
+    chain_res_us = time_steps(g_cr, g_cr1, args.steps, args.warmup, stream) * 1e3 / args.steps
+    del g_cr, g_cr1
+    # the FFN block with its residual connection fused into the down GEMM's epilogue
+    gf_multi = capture(lambda: [fused.step(r, stream, residual=True) for r in range(ROTATIONS)], stream)
+    gf_single = [capture(lambda r=r: fused.step(r, stream, residual=True), stream) for r in range(ROTATIONS)]
+    fused_res_us = time_steps(gf_multi, gf_single, args.steps, args.warmup, stream) * 1e3 / args.steps
     del gf_multi, gf_single, fused
     torch.cuda.empty_cache()
 
@@ -522,6 +536,9 @@ def run_fireq(args, rank, world, dev):
         "step_gbs": round(ffn.bytes_per_step() / (us_per_step * 1e-6) / 1e9, 1),
         "step_hbm_frac": round(ffn.bytes_per_step() / (us_per_step * 1e-6) / 1e9 / peaks["hbm_gbs"], 4),
         "fused_ffn_api_us": round(fused_us, 3),
+        "ffn_block_residual": {"fused_us": round(fused_res_us, 3), "unfused_chain_plus_add_us": round(chain_res_us, 3),
+                               "fused": "fireq_ffn_w4a8_decode: SwiGLU in gate_up's epilogue, residual in down's",
+                               "unfused": "the 4-kernel chain + y += x as its own kernel"},
         "roofline": {"bound": "hbm", "kernel": "fireq_w4a8_gemm gate_up M=16 N=22016 K=4096",
                      "achieved": round(gbs_gu, 1), "peak": hbm, "unit": "GB/s", "frac": round(gbs_gu / hbm, 4),
                      "traffic": traffic, "traffic_source": "stored: profiles/traffic.json, ncu --set full "

@@ -207,6 +207,22 @@ fireq_status_t fireq_w4a8_gemm_prefetch(const uint8_t* x_fp8, const void* x_scal
                                         const void* next_scales, size_t next_scales_bytes,
                                         void* stream);
 
+/*
+ * fireq_w4a8_gemm_residual -- fireq_w4a8_gemm (row-major Y) with Step 3's element-wise
+ * addition fused into the epilogue (Fig. 2 Step 3 "activation addition"; the
+ * residual connection around a Llama block):
+ *   Y[m][n] = BF16_RN( fp32(fp32(acc * (beta_m 2^-n)) * gamma_n) + R[m][n] )
+ * (gamma_n only when out_chan_scale is non-NULL; one BF16 rounding at the end).
+ *   residual  bf16 [M][ldr], ldr >= N, device, 16-byte aligned; may equal Y (in place).
+ * Everything else as fireq_w4a8_gemm with out_layout 0.  NULL residual ->
+ * FIREQ_ERROR_INVALID_VALUE.
+ */
+fireq_status_t fireq_w4a8_gemm_residual(const uint8_t* x_fp8, const void* x_scale, int64_t M, int64_t K,
+                                        const uint8_t* w_packed, const uint8_t* w_scales, int64_t N,
+                                        int32_t pts_exponent, const float* out_chan_scale,
+                                        const void* residual, int64_t ldr, void* Y, int64_t ldy,
+                                        void* workspace, size_t workspace_bytes, void* stream);
+
 /* --------------------------------------------------------- multi-GPU layer */
 /* Opaque NCCL communicator wrapper (caller-owned, not thread-safe). */
 typedef struct fireq_comm* fireq_comm_t;
@@ -334,15 +350,16 @@ fireq_status_t fireq_interleave_gate_up(const void* W_gate, const void* W_up, in
 size_t fireq_ffn_workspace_bytes(int64_t M, int64_t d_model, int64_t d_ff);
 
 /*
- * fireq_ffn_w4a8_decode -- a Llama FFN y = W_down (silu(W_gate x) * (W_up x))
- * at decode batch sizes as THREE kernels (vs four for the unfused chain):
+ * fireq_ffn_w4a8_decode -- a Llama FFN block y = W_down (silu(W_gate x) * (W_up x)) [+ r]
+ * at decode batch sizes with Step 3's element-wise operations fused into the
+ * GEMM epilogues, as four kernels:
  *   1. fireq_quantize_act(x, c_gu)                      (A1..A3, Eq. 2)
  *   2. gate_up GEMM over the interleaved W_gu (steps 1-3) whose epilogue forms
  *      h = bf16(silu(g) * u * c_down) from the bf16-rounded g and u (exactly
- *      fireq_silu_mul_quantize_act's x'), writes h and gathers the
- *      per-token max|h| with atomics; after a grid-wide barrier every CTA
- *      quantizes a slice of h with beta = bf16(amax / 448) (A2..A3);
- *   3. down GEMM on (h_hat, beta_h).
+ *      fireq_silu_mul_quantize_act's x') and writes h;
+ *   3. fireq_quantize_act(h)                            (A1..A3)
+ *   4. down GEMM on (h_hat, beta_h), residual added in its epilogue
+ *      (fireq_w4a8_gemm_residual) when residual != NULL.
  * Arguments
  *   x        bf16 [M][ldx], ldx >= d_model, ldx % 8 == 0.
  *   c_gu     bf16 [d_model]: CAS multiplier of W_gu (QuantizedWeight.c) or NULL.
@@ -350,24 +367,28 @@ size_t fireq_ffn_workspace_bytes(int64_t M, int64_t d_model, int64_t d_ff);
  *            (fireq_interleave_gate_up), N = 2 d_ff, K = d_model.
  *   c_down   bf16 [d_ff]: CAS multiplier of W_down (applied to u) or NULL.
  *   d_*      fireq_quantize_weight output for W_down, N = d_model, K = d_ff.
+ *   residual bf16 [M][ldr] (ldr >= d_model) added to y, or NULL; may equal x or y.
  *   h        out, bf16 [M][d_ff]: the SwiGLU output (before quantization).
  *   y        out, bf16 [M][ldy], ldy >= d_model.
  *   next_*   optional L2 prefetch of the next layer's weights (may be NULL).
  * Shapes: 1 <= M <= 16, d_model, d_ff multiples of 128; otherwise
  * FIREQ_ERROR_UNSUPPORTED_SHAPE.  Same arithmetic as the unfused chain
- * (quantize_act -> gemm -> silu_mul_quantize_act -> gemm) up to the fp32 summation
- * order of split tiles; y equals fireq_w4a8_gemm(quantize_act(h), W_down) exactly.
- * Environment FIREQ_FFN_PERSISTENT=1 (read once per process): ONE persistent launch
- * instead (x quantized in-kernel, three grid-wide barriers, the down phase scheduled
- * stream-K: y then equals the standalone down GEMM under FIREQ_NO_CSPLIT=1 exactly);
- * measured slower on B200, kept for the record.
+ * (quantize_act -> gemm -> silu_mul_quantize_act -> gemm[_residual]) up to the fp32
+ * summation order of split gate_up tiles; y equals
+ * fireq_w4a8_gemm[_residual](quantize_act(h), W_down) exactly.
+ * Environment (read once per process): FIREQ_FFN_MODE=3 -- three kernels, the gate_up
+ * kernel quantizing h in its tail behind a grid-wide barrier (per-token max|h| by
+ * atomics); FIREQ_FFN_PERSISTENT=1 -- ONE persistent launch (x quantized in-kernel,
+ * three grid-wide barriers, the down phase scheduled stream-K: y then equals the
+ * standalone down GEMM under FIREQ_NO_CSPLIT=1 exactly).  Both measured slower on B200
+ * and kept for the record.
  */
 fireq_status_t fireq_ffn_w4a8_decode(const void* x, int64_t ldx, const void* c_gu, int64_t M,
                                      int64_t d_model, int64_t d_ff, const uint8_t* gu_packed,
                                      const uint8_t* gu_scales, int32_t gu_pts, const void* c_down,
                                      const uint8_t* d_packed, const uint8_t* d_scales, int32_t d_pts,
-                                     void* h, void* y, int64_t ldy, void* workspace,
-                                     size_t workspace_bytes, const void* next_packed,
+                                     const void* residual, int64_t ldr, void* h, void* y, int64_t ldy,
+                                     void* workspace, size_t workspace_bytes, const void* next_packed,
                                      size_t next_packed_bytes, const void* next_scales,
                                      size_t next_scales_bytes, void* stream);
 

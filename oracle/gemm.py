@@ -42,8 +42,9 @@ def dequantize_weight(packed, scales, N, K):
     return E4M3_DECODE[table[sc_full, nib]]
 
 
-def gemm_reference(x_codes, beta, packed, scales, N, K, pts_n, gamma=None, w_deq=None):
-    """G2: r [M][N] float64."""
+def gemm_reference(x_codes, beta, packed, scales, N, K, pts_n, gamma=None, w_deq=None, residual=None):
+    """G2: r [M][N] float64.  residual (values [M][N]): Step 3's element-wise addition fused
+    into the epilogue ("activation function, addition ..."), r + R in fp64."""
     x = E4M3_DECODE[np.asarray(x_codes, dtype=np.uint8)]
     if w_deq is None:
         w_deq = dequantize_weight(packed, scales, N, K)
@@ -51,15 +52,19 @@ def gemm_reference(x_codes, beta, packed, scales, N, K, pts_n, gamma=None, w_deq
     r = acc * np.asarray(beta, dtype=np.float64)[:, None] * 2.0 ** (-pts_n)
     if gamma is not None:
         r = r * np.asarray(gamma, dtype=np.float64)[None, :]
+    if residual is not None:
+        r = r + np.asarray(residual, dtype=np.float64)
     return r
 
 
-def reference_rows(x_codes, beta, w_deq_rows, pts_n, gamma_rows=None):
+def reference_rows(x_codes, beta, w_deq_rows, pts_n, gamma_rows=None, residual_cols=None):
     """G2 for a subset of output channels (w_deq_rows [n_sel][K]) -- for sampled checks."""
     x = E4M3_DECODE[np.asarray(x_codes, dtype=np.uint8)]
     r = (x @ np.asarray(w_deq_rows).T) * np.asarray(beta, dtype=np.float64)[:, None] * 2.0 ** (-pts_n)
     if gamma_rows is not None:
         r = r * np.asarray(gamma_rows, dtype=np.float64)[None, :]
+    if residual_cols is not None:
+        r = r + np.asarray(residual_cols, dtype=np.float64)
     return r
 
 

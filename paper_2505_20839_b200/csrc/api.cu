@@ -32,7 +32,7 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
                          const float* gamma, __nv_bfloat16* Y, int64_t ldy, int out_layout, void* ws,
                          size_t ws_bytes, cudaStream_t stream, const void* pf0, size_t pf0_bytes,
                          const void* pf1, size_t pf1_bytes, __nv_bfloat16* const* peers = nullptr,
-                         int npeer = 0);
+                         int npeer = 0, const __nv_bfloat16* residual = nullptr, int64_t ldr = 0);
 fireq_status_t symm_signal_wait(unsigned* const* flag_ptrs, int nranks, int rank, cudaStream_t stream);
 fireq_status_t debug_lut_table(uint8_t* out, cudaStream_t stream);
 size_t ffn_workspace_bytes(int64_t M, int64_t d_model, int64_t d_ff);
@@ -40,7 +40,8 @@ bool ffn_shape_supported(int64_t M, int64_t d_model, int64_t d_ff);
 fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_bfloat16* c_gu, int64_t M,
                                int64_t d_model, int64_t d_ff, const uint8_t* gu_packed, const uint8_t* gu_scales,
                                int32_t gu_pts, const __nv_bfloat16* c_down, const uint8_t* d_packed,
-                               const uint8_t* d_scales, int32_t d_pts, __nv_bfloat16* h, __nv_bfloat16* y,
+                               const uint8_t* d_scales, int32_t d_pts, const __nv_bfloat16* residual,
+                               int64_t ldr, __nv_bfloat16* h, __nv_bfloat16* y,
                                int64_t ldy, void* ws, size_t ws_bytes, cudaStream_t stream, const void* pf0,
                                size_t pf0_bytes, const void* pf1, size_t pf1_bytes);
 fireq_status_t interleave_gate_up_impl(const __nv_bfloat16* wg, const __nv_bfloat16* wu, int64_t d_ff,
@@ -270,7 +271,7 @@ static fireq_status_t gemm_checked(const uint8_t* x_fp8, const void* x_scale, in
                                    const float* out_chan_scale, void* Y, int64_t ldy, int out_layout, void* workspace,
                                    size_t workspace_bytes, void* stream, const void* pf0, size_t pf0_bytes,
                                    const void* pf1, size_t pf1_bytes, __nv_bfloat16* const* peers = nullptr,
-                                   int npeer = 0) {
+                                   int npeer = 0, const void* residual = nullptr, int64_t ldr = 0) {
     FIREQ_NVTX("fireq_w4a8_gemm");
     FIREQ_REQUIRE(x_fp8 && x_scale && w_packed && w_scales && Y && workspace, FIREQ_ERROR_INVALID_VALUE,
                   "fireq_w4a8_gemm: NULL required pointer");
@@ -290,7 +291,8 @@ static fireq_status_t gemm_checked(const uint8_t* x_fp8, const void* x_scale, in
                   "fireq_w4a8_gemm_prefetch: prefetch regions must be 16-byte aligned");
     return gemm_impl(x_fp8, static_cast<const __nv_bfloat16*>(x_scale), M, K, w_packed, w_scales, N, pts_exponent,
                      out_chan_scale, static_cast<__nv_bfloat16*>(Y), ldy, out_layout, workspace, workspace_bytes,
-                     static_cast<cudaStream_t>(stream), pf0, pf0_bytes, pf1, pf1_bytes, peers, npeer);
+                     static_cast<cudaStream_t>(stream), pf0, pf0_bytes, pf1, pf1_bytes, peers, npeer,
+                     static_cast<const __nv_bfloat16*>(residual), ldr);
 }
 
 fireq_status_t fireq_w4a8_gemm(const uint8_t* x_fp8, const void* x_scale, int64_t M, int64_t K,
@@ -310,6 +312,17 @@ fireq_status_t fireq_w4a8_gemm_prefetch(const uint8_t* x_fp8, const void* x_scal
     return gemm_checked(x_fp8, x_scale, M, K, w_packed, w_scales, N, pts_exponent, out_chan_scale, Y, ldy, out_layout,
                         workspace, workspace_bytes, stream, next_packed, next_packed_bytes, next_scales,
                         next_scales_bytes);
+}
+
+fireq_status_t fireq_w4a8_gemm_residual(const uint8_t* x_fp8, const void* x_scale, int64_t M, int64_t K,
+                                        const uint8_t* w_packed, const uint8_t* w_scales, int64_t N,
+                                        int32_t pts_exponent, const float* out_chan_scale, const void* residual,
+                                        int64_t ldr, void* Y, int64_t ldy, void* workspace, size_t workspace_bytes,
+                                        void* stream) {
+    FIREQ_REQUIRE(residual, FIREQ_ERROR_INVALID_VALUE, "fireq_w4a8_gemm_residual: NULL residual");
+    FIREQ_REQUIRE(ldr >= N, FIREQ_ERROR_MISALIGNED, "fireq_w4a8_gemm_residual: ldr must be >= N");
+    return gemm_checked(x_fp8, x_scale, M, K, w_packed, w_scales, N, pts_exponent, out_chan_scale, Y, ldy, 0,
+                        workspace, workspace_bytes, stream, nullptr, 0, nullptr, 0, nullptr, 0, residual, ldr);
 }
 
 // ------------------------------------------------------------ fused decode FFN
@@ -333,9 +346,10 @@ fireq_status_t fireq_interleave_gate_up(const void* W_gate, const void* W_up, in
 fireq_status_t fireq_ffn_w4a8_decode(const void* x, int64_t ldx, const void* c_gu, int64_t M, int64_t d_model,
                                      int64_t d_ff, const uint8_t* gu_packed, const uint8_t* gu_scales, int32_t gu_pts,
                                      const void* c_down, const uint8_t* d_packed, const uint8_t* d_scales,
-                                     int32_t d_pts, void* h, void* y, int64_t ldy, void* workspace,
-                                     size_t workspace_bytes, const void* next_packed, size_t next_packed_bytes,
-                                     const void* next_scales, size_t next_scales_bytes, void* stream) {
+                                     int32_t d_pts, const void* residual, int64_t ldr, void* h, void* y,
+                                     int64_t ldy, void* workspace, size_t workspace_bytes, const void* next_packed,
+                                     size_t next_packed_bytes, const void* next_scales, size_t next_scales_bytes,
+                                     void* stream) {
     FIREQ_NVTX("fireq_ffn_w4a8_decode");
     FIREQ_REQUIRE(x && gu_packed && gu_scales && d_packed && d_scales && h && y && workspace, FIREQ_ERROR_INVALID_VALUE,
                   "fireq_ffn_w4a8_decode: NULL required pointer");
@@ -349,11 +363,13 @@ fireq_status_t fireq_ffn_w4a8_decode(const void* x, int64_t ldx, const void* c_g
     FIREQ_REQUIRE(aligned16(x) && (!c_gu || aligned16(c_gu)) && (!c_down || aligned16(c_down)) && aligned16(gu_packed) &&
                       aligned16(gu_scales) && aligned16(d_packed) && aligned16(d_scales) && aligned16(h) &&
                       aligned16(y) && ldx % 8 == 0 && ldx >= d_model && ldy % 8 == 0 && ldy >= d_model &&
-                      (!next_packed || aligned16(next_packed)) && (!next_scales || aligned16(next_scales)),
+                      (!next_packed || aligned16(next_packed)) && (!next_scales || aligned16(next_scales)) &&
+                      (!residual || ldr >= d_model),
                   FIREQ_ERROR_MISALIGNED, "fireq_ffn_w4a8_decode: pointers must be 16-byte aligned, ld % 8 == 0");
     return ffn_decode_impl(static_cast<const __nv_bfloat16*>(x), ldx, static_cast<const __nv_bfloat16*>(c_gu), M,
                            d_model, d_ff, gu_packed, gu_scales, gu_pts, static_cast<const __nv_bfloat16*>(c_down),
-                           d_packed, d_scales, d_pts, static_cast<__nv_bfloat16*>(h), static_cast<__nv_bfloat16*>(y),
+                           d_packed, d_scales, d_pts, static_cast<const __nv_bfloat16*>(residual), ldr,
+                           static_cast<__nv_bfloat16*>(h), static_cast<__nv_bfloat16*>(y),
                            ldy, workspace, workspace_bytes, static_cast<cudaStream_t>(stream), next_packed,
                            next_packed_bytes, next_scales, next_scales_bytes);
 }

@@ -92,6 +92,11 @@ struct GemmArgs {
     int64_t ldx_in;
     const __nv_bfloat16* x_chan; // c_k (nullable)
     uint8_t* xq_out;
+    // out_layout 0: residual added before the one BF16 rounding (Step 3's "addition"):
+    // y = bf16(acc * beta_m 2^-n [* gamma_n] + r[m][n]); r may alias Y (every element is read
+    // by the thread that computes it before any store of its 16-token chunk)
+    const __nv_bfloat16* residual;
+    int64_t ldr;
     unsigned long long* trace;   // debug timeline [C][8] (%globaltimer ns) or nullptr
     int dbg;                     // experiments only: bit0 skip conversion, bit1 skip MMAs, bit2 skip weight loads
     unsigned long long* span;    // profile builds: {start, end} of this launch
@@ -828,6 +833,9 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         const unsigned u_first = split_begin(blockIdx.x, a.U, a.Cs);
         int ntile = 0, m0 = 0, n = 0;
         float gam = 1.0f;
+        // residual of this thread's channel for the segment's first 16 tokens (bf16 pairs), loaded
+        // at the segment start so its L2 round trip overlaps the mainloop
+        uint32_t rpre[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         const bool use_gam = a.gamma != nullptr || (a.out_layout == 2 && a.gamma_up != nullptr);
         // Step 3 for 16 tokens [m0 + 16 ch, +16) of this thread's output channel n:
         // y = bf16(acc * (beta_m 2^-n) [* gamma_n]).  Y^T rows are 32 contiguous bytes per
@@ -835,13 +843,18 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         // whole 256-byte rows with 16-byte stores.
         auto emit = [&](const float (&acc)[16], int ch) {
             __align__(16) __nv_bfloat16 yb[16];
+            const int mb = m0 + ch * 16;
 #pragma unroll
             for (int c = 0; c < 16; ++c) {
                 float y = __fmul_rn(acc[c], sScale[ch * 16 + c]);
                 if (use_gam) y = __fmul_rn(y, gam);
+                if (a.residual && mb + c < a.M) {
+                    const float rv = ch == 0 ? __uint_as_float(((c & 1) ? (rpre[c >> 1] & 0xFFFF0000u) : (rpre[c >> 1] << 16)))
+                                             : __bfloat162float(a.residual[(size_t)(mb + c) * a.ldr + n]);
+                    y = __fadd_rn(y, rv);
+                }
                 yb[c] = __float2bfloat16_rn(y);
             }
-            const int mb = m0 + ch * 16;
             if (a.out_layout == 1) {
                 for (int p = 0; p < (a.npeer > 1 ? a.npeer : 1); ++p) {
                     __nv_bfloat16* dst = (a.npeer > 1 ? a.Yp[p] : a.Y) + (size_t)n * a.ldy + mb;
@@ -872,8 +885,10 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                         a.h_out[(size_t)m * a.ldh + ch_out] = hb;
                         hm = fabsf(__bfloat162float(hb));
                     }
-                    for (int o = 16; o; o >>= 1) hm = fmaxf(hm, __shfl_xor_sync(0xffffffffu, hm, o));
-                    if (lane == 0 && m < a.M) atomicMax(a.amax_out + m, __float_as_uint(hm));
+                    if (a.amax_out) {
+                        for (int o = 16; o; o >>= 1) hm = fmaxf(hm, __shfl_xor_sync(0xffffffffu, hm, o));
+                        if (lane == 0 && m < a.M) atomicMax(a.amax_out + m, __float_as_uint(hm));
+                    }
                 }
                 ptx::named_bar_sync(1, 128);
             } else {
@@ -910,6 +925,16 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                 gam = (r < 64 || !a.gamma_up) ? 1.0f : __bfloat162float(a.gamma_up[ntile * 64 + (r - 64)]);
             else
                 gam = a.gamma ? a.gamma[n] : 1.0f;
+            if (a.residual) {
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    uint32_t v = 0u;
+                    // (asm volatile: issued here, not sunk to the use after the accumulator wait)
+                    if (m0 + c < a.M)
+                        asm volatile("ld.global.nc.u16 %0, [%1];" : "=r"(v) : "l"(a.residual + (size_t)(m0 + c) * a.ldr + n));
+                    rpre[c >> 1] = (c & 1) ? (rpre[c >> 1] | (v << 16)) : v;
+                }
+            }
             sScale = sScaleBuf + (sg & 1) * 256;
             for (int t = r; t < NTOK; t += 128)
                 sScale[t] = (m0 + t < a.M) ? __fmul_rn(__bfloat162float(a.x_scale[m0 + t]), p2) : 0.0f;
@@ -1704,7 +1729,8 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
                          const uint8_t* w_packed, const uint8_t* w_scales, int64_t N, int32_t pts_n,
                          const float* gamma, __nv_bfloat16* Y, int64_t ldy, int out_layout, void* ws,
                          size_t ws_bytes, cudaStream_t stream, const void* pf0, size_t pf0_bytes,
-                         const void* pf1, size_t pf1_bytes, __nv_bfloat16* const* peers, int npeer) {
+                         const void* pf1, size_t pf1_bytes, __nv_bfloat16* const* peers, int npeer,
+                         const __nv_bfloat16* residual, int64_t ldr) {
     const Plan p = make_plan(M, N, K);
     if (ws_bytes < gemm_workspace_bytes(M, N, K)) return fail(FIREQ_ERROR_WORKSPACE, "GEMM workspace too small");
     CUtensorMap map;
@@ -1715,6 +1741,8 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
     args.Y = Y;
     args.ldy = ldy;
     args.out_layout = out_layout;
+    args.residual = residual;
+    args.ldr = ldr;
     args.npeer = 0;
     if (peers && npeer > 1) {
         if (npeer > 8 || out_layout != 1) return fail(FIREQ_ERROR_INVALID_VALUE, "peer stores: Y^T and <= 8 ranks");
@@ -1766,19 +1794,24 @@ fireq_status_t quantize_act_impl(const __nv_bfloat16* X, const __nv_bfloat16* U,
 fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_bfloat16* c_gu, int64_t M,
                                int64_t d_model, int64_t d_ff, const uint8_t* gu_packed, const uint8_t* gu_scales,
                                int32_t gu_pts, const __nv_bfloat16* c_down, const uint8_t* d_packed,
-                               const uint8_t* d_scales, int32_t d_pts, __nv_bfloat16* h, __nv_bfloat16* y,
+                               const uint8_t* d_scales, int32_t d_pts, const __nv_bfloat16* residual,
+                               int64_t ldr, __nv_bfloat16* h, __nv_bfloat16* y,
                                int64_t ldy, void* ws, size_t ws_bytes, cudaStream_t stream, const void* pf0,
                                size_t pf0_bytes, const void* pf1, size_t pf1_bytes) {
     if (!ffn_shape_supported(M, d_model, d_ff))
         return fail(FIREQ_ERROR_UNSUPPORTED_SHAPE, "fused FFN: decode batches (M <= 16) only");
     if (ws_bytes < ffn_workspace_bytes(M, d_model, d_ff)) return fail(FIREQ_ERROR_WORKSPACE, "FFN workspace too small");
-    // Default: three kernels (act quant; gate_up with the SwiGLU tail; down with its own best
-    // plan, cluster split-K at decode).  FIREQ_FFN_PERSISTENT=1: ONE persistent launch (NPH = 2):
+    // Default: four kernels -- act quant(x); gate_up whose epilogue forms h = bf16(silu(g) u);
+    // act quant(h) (one CTA per token row: its amax reduction stays inside the CTA); down with
+    // its own best plan (cluster split-K at decode) and the residual added in its epilogue.
+    // FIREQ_FFN_MODE=3: three kernels (the gate_up kernel quantizes h in its tail behind a
+    // grid barrier, per-token max|h| by atomics).  FIREQ_FFN_PERSISTENT=1: ONE persistent launch (NPH = 2):
     // x quantized in-kernel (phase A, grid barrier), gate_up with the SwiGLU epilogue, grid
     // barrier, each CTA quantizing a 1/C slice of h, grid barrier, down (stream-K for both
     // phases).  Measured slower (41.5 vs 35.2 us for the Llama2-7B FFN): each phase boundary
     // is ~6 serialized global round trips of ~0.7 us under load (fused decode FFN).
     static const bool split = getenv("FIREQ_FFN_PERSISTENT") == nullptr;
+    static const bool tail_quant = getenv("FIREQ_FFN_MODE") && atoi(getenv("FIREQ_FFN_MODE")) == 3;
     const Plan p1 = make_plan(M, 2 * d_ff, d_model, false), p2 = make_plan(M, d_model, d_ff, split);
     uint8_t* w = static_cast<uint8_t*>(ws);
     uint8_t* ws1 = w;
@@ -1810,6 +1843,8 @@ fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_b
     a2.Y = y;
     a2.ldy = ldy;
     a2.out_layout = 0;
+    a2.residual = residual;
+    a2.ldr = ldr;
 #if FIREQ_PROFILE
     static const int trace_which = getenv("FIREQ_TRACE_WHICH") ? atoi(getenv("FIREQ_TRACE_WHICH")) : 0;  // debug
     if (trace_which == 2) a1.trace = nullptr;
@@ -1825,6 +1860,15 @@ fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_b
     }
     fireq_status_t st = quantize_act_impl(x, nullptr, M, d_model, ldx, c_gu, c_gu ? 1 : 0, false, xq, xbeta, stream);
     if (st != FIREQ_SUCCESS) return st;
+    if (!tail_quant) {
+        a1.amax_out = nullptr;               // the act-quant kernel reduces each row itself
+        a1.hq_out = nullptr;
+        st = launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map1, a1, stream);
+        if (st != FIREQ_SUCCESS) return st;
+        st = quantize_act_impl(h, nullptr, M, d_ff, d_ff, nullptr, 0, false, hq, hbeta, stream);
+        if (st != FIREQ_SUCCESS) return st;
+        return launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map2, a2, stream);
+    }
     st = launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map1, a1, stream);
     if (st != FIREQ_SUCCESS) return st;
     return launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map2, a2, stream);

@@ -78,8 +78,9 @@ def load(path=LIB_PATH):
         "fireq_debug_set_spans": ([P, C], C),
         "fireq_interleave_gate_up": ([P, P, I64, I64, P, P], C),
         "fireq_ffn_workspace_bytes": ([I64, I64, I64], SZ),
-        "fireq_ffn_w4a8_decode": ([P, I64, P, I64, I64, I64, P, P, I32, P, P, P, I32, P, P, I64, P, SZ, P, SZ, P, SZ,
-                                   P], C),
+        "fireq_ffn_w4a8_decode": ([P, I64, P, I64, I64, I64, P, P, I32, P, P, P, I32, P, I64, P, P, I64, P, SZ, P, SZ,
+                                   P, SZ, P], C),
+        "fireq_w4a8_gemm_residual": ([P, P, I64, I64, P, P, I64, I32, P, P, I64, P, I64, P, SZ, P], C),
     }
     for name, (args, res) in sig.items():
         if os.environ.get("FIREQ_LOAD_PARTIAL") and not hasattr(lib, name):   # bisecting older builds
@@ -265,11 +266,13 @@ class Workspace:
 
 
 def w4a8_gemm(xq, beta, packed, scales, N, pts_n, gamma=None, out=None, out_layout=0, workspace=None,
-              stream=None, prefetch=None):
+              stream=None, prefetch=None, residual=None):
     """Y = fireq_w4a8_gemm(...): bf16 [M][N] (out_layout 0) or [N][M] (out_layout 1).
 
     prefetch: optional (next_packed, next_scales) uint8 tensors of the next layer, streamed
     into L2 once this GEMM's own weight loads are issued (fireq_w4a8_gemm_prefetch).
+    residual: optional bf16 [M][>= N] added before the BF16 rounding (fireq_w4a8_gemm_residual,
+    row-major Y only; may be `out` itself).
     """
     M, K = xq.shape
     L = lib()
@@ -278,7 +281,13 @@ def w4a8_gemm(xq, beta, packed, scales, N, pts_n, gamma=None, out=None, out_layo
     if out is None:
         out = torch.empty((M, N) if out_layout == 0 else (N, M), dtype=torch.bfloat16, device=xq.device)
     ldy = out.stride(0)
-    if prefetch is None:
+    if residual is not None:
+        if out_layout != 0 or prefetch is not None:
+            raise FireqError("w4a8_gemm: residual needs out_layout 0 and no prefetch")
+        _check(L.fireq_w4a8_gemm_residual(_ptr(xq), _ptr(beta), M, K, _ptr(packed), _ptr(scales), N, pts_n,
+                                          _ptr(gamma), _ptr(residual), residual.stride(0), _ptr(out), ldy, _ptr(ws),
+                                          ws.numel(), _stream(stream)), "fireq_w4a8_gemm_residual")
+    elif prefetch is None:
         _check(L.fireq_w4a8_gemm(_ptr(xq), _ptr(beta), M, K, _ptr(packed), _ptr(scales), N, pts_n, _ptr(gamma),
                                  _ptr(out), ldy, out_layout, _ptr(ws), ws.numel(), _stream(stream)), "fireq_w4a8_gemm")
     else:
@@ -305,8 +314,8 @@ def ffn_workspace_bytes(M, d_model, d_ff):
     return lib().fireq_ffn_workspace_bytes(M, d_model, d_ff)
 
 
-def ffn_w4a8_decode(x, q_gu, q_d, h=None, out=None, workspace=None, stream=None, prefetch=None):
-    """y = fireq_ffn_w4a8_decode(x, ...): the two-kernel fused decode FFN.
+def ffn_w4a8_decode(x, q_gu, q_d, h=None, out=None, workspace=None, stream=None, prefetch=None, residual=None):
+    """y = fireq_ffn_w4a8_decode(x, ...) [+ residual]: the fused decode FFN block.
 
     q_gu: QuantizedWeight of the interleaved W_gu (interleave_gate_up); q_d: of W_down.
     workspace: Workspace of ffn_workspace_bytes (zeroed once, left zeroed by each call).
@@ -323,6 +332,7 @@ def ffn_w4a8_decode(x, q_gu, q_d, h=None, out=None, workspace=None, stream=None,
     pp, ps = prefetch if prefetch is not None else (None, None)
     _check(L.fireq_ffn_w4a8_decode(_ptr(x), x.stride(0), _ptr(q_gu.c), M, d_model, d_ff, _ptr(q_gu.packed),
                                    _ptr(q_gu.scales), q_gu.n, _ptr(q_d.c), _ptr(q_d.packed), _ptr(q_d.scales), q_d.n,
+                                   _ptr(residual), residual.stride(0) if residual is not None else 0,
                                    _ptr(h), _ptr(out), out.stride(0), _ptr(ws), ws.numel(),
                                    _ptr(pp), pp.numel() if pp is not None else 0,
                                    _ptr(ps), ps.numel() if ps is not None else 0, _stream(stream)),

@@ -6,13 +6,15 @@ from paper_2505_20839_b200 import fireq as F
 F.load(os.path.join(os.path.dirname(F.LIB_PATH), 'libfireq_prof.so'))
 import bench
 dev = torch.device("cuda", 0)
-ffn = bench.FFN(F, 16, 4, dev)
+FUSED = os.environ.get("FUSED") == "1"
+ffn = bench.FusedFFN(F, 16, 4, dev) if FUSED else bench.FFN(F, 16, 4, dev)
 stream = torch.cuda.Stream()
 for r in range(8):
     with torch.cuda.stream(stream):
         ffn.step(r % 4, stream)
 torch.cuda.synchronize()
-names = ["act_quant(x)", "gemm gate_up", "silu_mul_quant", "gemm down"]
+names = (["act_quant(x)", "gemm gate_up+SwiGLU", "act_quant(h)", "gemm down"] if FUSED else
+         ["act_quant(x)", "gemm gate_up", "silu_mul_quant", "gemm down"])
 buf = torch.zeros((4 * 3, 2), dtype=torch.int64, device=dev)
 F.debug_set_spans(buf)
 g = torch.cuda.CUDAGraph()

@@ -18,10 +18,12 @@ for M, N, K in zip(args[0::3], args[1::3], args[2::3]):
     rot = [(qw.packed.clone(), qw.scales.clone()) for _ in range(ROT)]
     ws = F.Workspace(F.gemm_workspace_bytes(M, N, K))
     out = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+    gam = torch.rand(N, device="cuda") + 0.5 if os.environ.get("GAMMA") else None
+    res = torch.randn((M, N), device="cuda").bfloat16() if os.environ.get("RESIDUAL") else None
     s = torch.cuda.Stream()
     def run():
         for p, sc in rot:
-            F.w4a8_gemm(xq, beta, p, sc, N, qw.n, out=out, workspace=ws, stream=s)
+            F.w4a8_gemm(xq, beta, p, sc, N, qw.n, gamma=gam, out=out, workspace=ws, stream=s, residual=res)
     with torch.cuda.stream(s):
         run()
     torch.cuda.synchronize()

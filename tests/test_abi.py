@@ -70,9 +70,15 @@ def test_fused_ffn_host_checks(lib):
     assert lib.fireq_ffn_workspace_bytes(16, 4000, 11008) == 0          # not a multiple of 128
     buf = ctypes.create_string_buffer(1 << 12)
     a16 = P((ctypes.addressof(buf) + 15) & ~15)
-    args = lambda M, x: (x, 4096, None, M, 4096, 11008, a16, a16, 0, None, a16, a16, 0, a16, a16, 4096, a16,
-                         1 << 20, None, 0, None, 0, None)
+    args = lambda M, x: (x, 4096, None, M, 4096, 11008, a16, a16, 0, None, a16, a16, 0, None, 0, a16, a16, 4096,
+                         a16, 1 << 20, None, 0, None, 0, None)
     assert lib.fireq_ffn_w4a8_decode(*args(16, None)) == 1               # NULL x
     assert lib.fireq_ffn_w4a8_decode(*args(17, a16)) == 2                # decode only: M <= 16
     assert lib.fireq_ffn_w4a8_decode(*args(16, P(a16.value + 2))) == 3  # misaligned x
+    bad_r = list(args(16, a16)); bad_r[13] = a16; bad_r[14] = 100         # residual with ldr < d_model
+    assert lib.fireq_ffn_w4a8_decode(*bad_r) == 3
+    # fireq_w4a8_gemm_residual: NULL residual / ldr < N
+    g = lambda r, ldr: lib.fireq_w4a8_gemm_residual(a16, a16, 16, 4096, a16, a16, 4096, 0, None, r, ldr, a16, 4096,
+                                                    a16, 1 << 20, None)
+    assert g(None, 4096) == 1 and g(a16, 100) == 3
     assert lib.fireq_interleave_gate_up(a16, a16, 100, 4096, a16, None) == 2

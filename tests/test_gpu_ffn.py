@@ -124,9 +124,13 @@ def _check_fused(fireq, M, d, dff, seed, reps=3):
     ys = [fireq.ffn_w4a8_decode(x, qil, qd, h=h, workspace=ws) for _ in range(reps)]
     hq2, hb2 = fireq.quantize_act(h)
     y2 = fireq.w4a8_gemm(hq2, hb2, qd.packed, qd.scales, d, qd.n)
+    # the FFN block with its residual connection: y + x in the down GEMM's epilogue
+    yr = fireq.ffn_w4a8_decode(x, qil, qd, h=h, workspace=ws, residual=x)
+    yr2 = fireq.w4a8_gemm(hq2, hb2, qd.packed, qd.scales, d, qd.n, residual=x)
     torch.cuda.synchronize()
     assert all(torch.equal(v, ys[0]) for v in ys)
     assert torch.equal(ys[0], y2), (ys[0].float() - y2.float()).abs().max().item()
+    assert torch.equal(yr, yr2)
     # h of the interleaved gate_up vs the plain one: same up to the fp32 summation order of
     # split tiles (the two paths schedule gate_up differently)
     assert torch.allclose(hb2.float(), hb.float(), rtol=2 ** -7, atol=0)
@@ -152,11 +156,19 @@ FUSED_CASES = [(16, 1024, 2816), (5, 512, 384), (1, 256, 128), (11, 768, 1280), 
 
 
 @pytest.mark.parametrize("M,d,dff", FUSED_CASES)
-def test_fused_ffn_three_kernels(fireq, M, d, dff):
-    """Default fireq_ffn_w4a8_decode: quantize_act(x); gate_up with the SwiGLU tail; down with
-    the standalone GEMM's own plan (cluster split-K at decode) -- y equals it bit for bit.
-    (4096 x 11008: Llama2-7B, 8 back-to-back calls.)"""
+def test_fused_ffn_default(fireq, M, d, dff):
+    """Default fireq_ffn_w4a8_decode: quantize_act(x); gate_up whose epilogue forms h; quantize_act(h);
+    down with the standalone GEMM's own plan (cluster split-K at decode) and the residual in its
+    epilogue -- y equals fireq_w4a8_gemm[_residual](quantize_act(h)) bit for bit.  (4096 x 11008:
+    Llama2-7B, 8 back-to-back calls.)"""
     _check_fused(fireq, M, d, dff, 71 + M, reps=8 if d == 4096 else 3)
+
+
+@pytest.mark.parametrize("M,d,dff", [(16, 1024, 2816), (16, 4096, 11008)])
+def test_fused_ffn_tail_quant_mode(M, d, dff):
+    """FIREQ_FFN_MODE=3: the gate_up kernel quantizes h in its tail (grid barrier, max|h| by
+    atomics); same bit-exact checks."""
+    _isolated("T._check_fused(F, %d, %d, %d, %d)" % (M, d, dff, 271 + M), {"FIREQ_FFN_MODE": "3"})
 
 
 @pytest.mark.parametrize("M,d,dff", [(16, 1024, 2816), (5, 512, 384), (16, 4096, 11008)])
@@ -171,14 +183,17 @@ def test_fused_ffn_single_launch(M, d, dff):
               {"FIREQ_NO_CSPLIT": "1", "FIREQ_FFN_PERSISTENT": "1"})
 
 
-def test_fused_ffn_vs_oracle(fireq):
+@pytest.mark.parametrize("with_residual", [False, True])
+def test_fused_ffn_vs_oracle(fireq, with_residual):
     M, d, dff = 16, 1024, 2816
     wg, wu, wd, xb, *_, qil, qd, x = _ffn_case(fireq, M, d, dff, 81)
-    y = fireq.ffn_w4a8_decode(x, qil, qd, workspace=fireq.Workspace(fireq.ffn_workspace_bytes(M, d, dff)))
+    y = fireq.ffn_w4a8_decode(x, qil, qd, workspace=fireq.Workspace(fireq.ffn_workspace_bytes(M, d, dff)),
+                              residual=x if with_residual else None)
     torch.cuda.synchronize()
     ref_gu = oq.quantize_weight(synth.bits_to_f64(np.concatenate([wg, wu], axis=0)), 1)
     ref_d = oq.quantize_weight(synth.bits_to_f64(wd), 1)
-    _, r = of.ffn_reference(synth.bits_to_f64(xb), ref_gu, ref_d, dff)
+    _, r = of.ffn_reference(synth.bits_to_f64(xb), ref_gu, ref_d, dff,
+                            residual=synth.bits_to_f64(xb) if with_residual else None)
     yv = y.float().cpu().numpy().astype(np.float64)
     assert og.g4_error(yv, r) <= 2e-2                        # same bound as the unfused chain
     assert og.rel_frobenius(yv, r) < 5e-3

@@ -198,6 +198,32 @@ def test_gemm_g4(fireq, M, N, K):
     assert og.rel_frobenius(y, r) < 5e-3
 
 
+@pytest.mark.parametrize("M,N,K", [
+    (16, 10240, 256),        # stream-K (contributors' partials summed by the tile owner)
+    (16, 4096, 1280),        # cluster split-K (DSMEM reduction in rank 0)
+    (128, 1024, 2048),       # cluster split-K reduce-scatter (each rank emits its token chunks)
+    (5, 128, 640),           # one tile over 5 CTAs
+    (300, 512, 384),         # whole tiles, ragged m-tile
+])
+def test_gemm_residual(fireq, M, N, K):
+    """fireq_w4a8_gemm_residual (Step 3's addition): G4 against the oracle's
+    r + R in fp64; in place (R is Y) equals out of place bit for bit; a zero residual
+    leaves every output as the plain GEMM's (x + 0 = x in fp32)."""
+    y, r, qw, xq, beta = run_case(fireq, M, N, K, seed=7 * M + N)
+    rb = synth.activations(M, N, synth.layer_seed(9, M + N))
+    R = to_dev_bf16(rb)
+    Y = fireq.w4a8_gemm(xq, beta, qw.packed, qw.scales, N, qw.n, residual=R)
+    Y2 = R.clone()
+    fireq.w4a8_gemm(xq, beta, qw.packed, qw.scales, N, qw.n, residual=Y2, out=Y2)
+    Y0 = fireq.w4a8_gemm(xq, beta, qw.packed, qw.scales, N, qw.n, residual=torch.zeros_like(R))
+    torch.cuda.synchronize()
+    rr = r + synth.bits_to_f64(rb)
+    yv = Y.float().cpu().numpy().astype(np.float64)
+    assert og.g4_error(yv, rr) <= G4_TOL and og.rel_frobenius(yv, rr) < 5e-3
+    assert torch.equal(Y, Y2)
+    assert np.array_equal(Y0.float().cpu().numpy().astype(np.float64), y)
+
+
 @pytest.mark.parametrize("M,N,K,mode", [
     (16, 10240, 256, "stream-k"),            # 80 tiles: stream-K remainder over all CTAs
     (16, 4096, 1280, "cluster-split-k"),     # 32 tiles x 4-CTA clusters, ragged K split (10 / 4)

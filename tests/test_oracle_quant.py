@@ -366,6 +366,32 @@ def test_gemm_reference_vs_fraction_bruteforce():
         assert abs(F(float(r[m, n])) - exact) <= abs(exact) * F(1, 2 ** 50)
 
 
+def test_gemm_reference_residual():
+    """Step 3's fused addition: the exact-rational brute force of one output plus the
+    residual value; and an all-zero weight gives exactly the residual (zero groups: sigma = 0,
+    every LUT entry 0)."""
+    rng = np.random.default_rng(12)
+    N, K, M = 128, 256, 2
+    W = nm.bf16_rn(rng.standard_normal((N, K)) * 0.02)
+    q = quant.quantize_weight(W, 1)
+    X = nm.bf16_rn(rng.standard_normal((M, K)))
+    R = nm.bf16_rn(rng.standard_normal((M, N)))
+    xc, beta = quant.quantize_act(X, q.c)
+    r = gemm.gemm_reference(xc, beta, q.packed, q.scales, N, K, q.n, residual=R)
+    codes = layout.unpack_codes(q.packed, N, K)
+    scodes = layout.unpack_scales(q.scales, N, K)
+    from test_oracle_numerics import rn_exact
+    for (m, n) in [(0, 3), (1, 100)]:
+        acc = F(0)
+        for k in range(K):
+            acc += F(float(nm.E4M3_DECODE[xc[m, k]])) * rn_exact(int(codes[n, k]) * GRID[scodes[n, k // 128]])
+        exact = acc * F(float(beta[m])) / F(2) ** q.n + F(float(R[m, n]))
+        assert abs(F(float(r[m, n])) - exact) <= abs(exact) * F(1, 2 ** 50)
+    q0 = quant.quantize_weight(np.zeros((N, K)), 0)
+    r0 = gemm.gemm_reference(xc, beta, q0.packed, q0.scales, N, K, q0.n, residual=R)
+    assert np.array_equal(r0, R)
+
+
 def test_gemm_exactness_corridor_and_zero_groups():
     # integer operands, sigma = 1, beta = 1, n = 0: reference is an exact integer dot product
     rng = np.random.default_rng(11)
