@@ -392,6 +392,48 @@ fireq_status_t fireq_ffn_w4a8_decode(const void* x, int64_t ldx, const void* c_g
                                      size_t next_packed_bytes, const void* next_scales,
                                      size_t next_scales_bytes, void* stream);
 
+/* ------------------------------------------------------ KV4Q8 attention (NEXT f4) */
+/*
+ * fireq_quantize_kv -- one head's INT4 KV-cache block (DESIGN R30-R35):
+ * X bf16 [N][d] (contiguous; N, d multiples of 128) quantized exactly as fireq_quantize_weight
+ * with a CALLER-GIVEN per-column multiplier in place of CAS: X_bar = fp32(X) * lambda_k
+ * (lambda = 1/t for the post-RoPE key channels CRS rescales; NULL = 1), PTS exponent
+ * n (W3), 128-groups along each row with RZ FP8 scales (W4-W6), layout v1.
+ *   keys:   X = K_post of one (sequence, kv head) [N tokens][d]  -> one group per token row
+ *   values: X = V^T of one (sequence, kv head) [d][N tokens]      -> groups of 128 tokens
+ * pts_and_status: device int32[2] {n, status} as fireq_quantize_weight.
+ * workspace >= fireq_quantize_weight_workspace_bytes(N, d).
+ */
+fireq_status_t fireq_quantize_kv(const void* X, int64_t N, int64_t d, const float* chan_lambda,
+                                 uint8_t* packed, uint8_t* scales, int32_t* pts_and_status,
+                                 void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * fireq_kv4q8_attention -- prefill self-attention with FP8 queries and the INT4 KV cache
+ * (KV4Q8-FP; S = Q K^T and O = P V through the INT4 x FP8 path; softmax
+ * quantized to FP8; the three-stage overlap of Alg. 1 P:227-291 on tcgen05):
+ *   S[q][k]  = beta_q[q] 2^-n_k sum_c dec(q_hat[q][c]) LUT_k(K[k][c])      (FP32 accumulation)
+ *   x        = tau S,  causal: k > q excluded;  m = max_k x;  P = exp(x - m);  l = sum_k P
+ *   P_hat    = E4M3_RN(448 P)
+ *   O[q][c]  = BF16( 2^-n_v / 448 / l * sum_k dec(P_hat[q][k]) LUT_v(V^T[c][k]) )
+ * Arguments (device pointers)
+ *   q_fp8    E4M3 [B][Hq][N][d] (fireq_quantize_act per (token, head) row, post-RoPE, CRS
+ *            multiplier c = t applied as A1's channel multiplier), q_scale bf16 [B][Hq][N].
+ *   k_*      [B][Hkv] consecutive fireq_quantize_kv outputs of K_post [N][d]
+ *            (packed N d / 2 bytes, scales N d / 128 bytes per head), k_pts int32 [B][Hkv][2].
+ *   vt_*     [B][Hkv] consecutive fireq_quantize_kv outputs of V^T [d][N], v_pts likewise.
+ *   d = 128, N % 128 == 0, Hq % Hkv == 0 (grouped-query: q head h reads kv head h / (Hq/Hkv)).
+ *   causal   1 = causal mask; tau > 0 (usually 1/sqrt(d)).
+ *   O        out, bf16 [B N][ldo] (token-major, head h at columns [h d, h d + d): the o_proj
+ *            input), ldo >= Hq d, ldo % 8 == 0.
+ */
+fireq_status_t fireq_kv4q8_attention(const uint8_t* q_fp8, const void* q_scale, int64_t B, int64_t N,
+                                     int64_t Hq, int64_t Hkv, int64_t d, const uint8_t* k_packed,
+                                     const uint8_t* k_scales, const int32_t* k_pts,
+                                     const uint8_t* vt_packed, const uint8_t* vt_scales,
+                                     const int32_t* v_pts, int causal, float tau, void* O, int64_t ldo,
+                                     void* stream);
+
 /* The schedule fireq_w4a8_gemm chooses for (M, N, K), for benchmarks and tests:
  * writes {ntok, mode, ctas, sign_split} into cfg_out[4] (host).  mode 0 = whole
  * tiles, 1 = whole tiles + stream-K remainder (global-memory fixup), 2 = cluster

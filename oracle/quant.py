@@ -35,6 +35,14 @@ PTS_MAX_N = 60
 
 
 # --------------------------------------------------------------------- W1 / W2
+def given_lambda(lam):
+    """W1 with a caller-given per-input-channel multiplier (the KV-cache path: CRS divides the
+    post-RoPE outlier key channels by t, lambda = fp32(1 / t)): c = bf16(1/lambda)."""
+    lam = np.asarray(lam, dtype=np.float32).astype(np.float64)
+    c = bf16_rn((np.float32(1.0) / lam.astype(np.float32)).astype(np.float64))
+    return lam, c
+
+
 def cas_lambda(W, cas_mode):
     """W1: per-input-channel lambda (fp32 values as float64) and c = bf16(1/lambda).
 
@@ -163,7 +171,7 @@ class QuantizedWeight:
         self.__dict__.update(kw)
 
 
-def quantize_weight(W, cas_mode, pack=True, rows=None):
+def quantize_weight(W, cas_mode, pack=True, rows=None, lam=None):
     """W1-W6 for a bf16 weight matrix W [N][K] (float64 array of bf16 values).
 
     pack=False skips W6 (packed/scales are None) for large sampled checks.
@@ -181,7 +189,7 @@ def quantize_weight(W, cas_mode, pack=True, rows=None):
         raise ValueError("N and K must be multiples of 128")
     if not np.all(np.isfinite(W)):
         raise ValueError("non-finite weight")
-    lam, c = cas_lambda(W, cas_mode)
+    lam, c = cas_lambda(W, cas_mode) if lam is None else given_lambda(lam)
     W_bar = cas_apply(W, lam)
     n, reason = pts_exponent(W_bar)
     if rows is not None:

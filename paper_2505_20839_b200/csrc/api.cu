@@ -46,6 +46,12 @@ fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_b
                                size_t pf0_bytes, const void* pf1, size_t pf1_bytes);
 fireq_status_t interleave_gate_up_impl(const __nv_bfloat16* wg, const __nv_bfloat16* wu, int64_t d_ff,
                                        int64_t d_model, __nv_bfloat16* out, cudaStream_t stream);
+fireq_status_t kv4q8_attention_impl(const uint8_t* q_fp8, const __nv_bfloat16* q_scale, const uint8_t* k_packed,
+                                    const uint8_t* k_scales, const int32_t* k_pts, const uint8_t* vt_packed,
+                                    const uint8_t* vt_scales, const int32_t* v_pts, int64_t B, int64_t N,
+                                    int64_t Hq, int64_t Hkv, int causal, float tau, __nv_bfloat16* O, int64_t ldo,
+                                    cudaStream_t stream);
+
 extern unsigned long long* g_trace;
 void clear_x_map_cache();
 
@@ -323,6 +329,44 @@ fireq_status_t fireq_w4a8_gemm_residual(const uint8_t* x_fp8, const void* x_scal
     FIREQ_REQUIRE(ldr >= N, FIREQ_ERROR_MISALIGNED, "fireq_w4a8_gemm_residual: ldr must be >= N");
     return gemm_checked(x_fp8, x_scale, M, K, w_packed, w_scales, N, pts_exponent, out_chan_scale, Y, ldy, 0,
                         workspace, workspace_bytes, stream, nullptr, 0, nullptr, 0, nullptr, 0, residual, ldr);
+}
+
+// ------------------------------------------------------------ KV4 cache quantizer
+fireq_status_t fireq_quantize_kv(const void* X, int64_t N, int64_t d, const float* chan_lambda, uint8_t* packed,
+                                 uint8_t* scales, int32_t* pts_and_status, void* workspace, size_t workspace_bytes,
+                                 void* stream) {
+    FIREQ_NVTX("fireq_quantize_kv");
+    FIREQ_REQUIRE(X && packed && scales && pts_and_status && workspace, FIREQ_ERROR_INVALID_VALUE,
+                  "fireq_quantize_kv: NULL required pointer");
+    FIREQ_REQUIRE(N >= 128 && N % 128 == 0 && d >= 128 && d % 128 == 0 && N <= (int64_t(1) << 20) && d <= 65536,
+                  FIREQ_ERROR_UNSUPPORTED_SHAPE, "fireq_quantize_kv: N and d must be multiples of 128");
+    FIREQ_REQUIRE(workspace_bytes >= wq_workspace_bytes(d), FIREQ_ERROR_WORKSPACE, "fireq_quantize_kv: workspace too small");
+    FIREQ_REQUIRE(aligned16(X) && aligned16(packed) && aligned16(scales) && (!chan_lambda || aligned16(chan_lambda)),
+                  FIREQ_ERROR_MISALIGNED, "fireq_quantize_kv: pointers must be 16-byte aligned");
+    return quantize_weight_impl(static_cast<const __nv_bfloat16*>(X), N, d, 2, packed, scales,
+                                const_cast<float*>(chan_lambda), nullptr, pts_and_status, workspace,
+                                static_cast<cudaStream_t>(stream), false);
+}
+
+fireq_status_t fireq_kv4q8_attention(const uint8_t* q_fp8, const void* q_scale, int64_t B, int64_t N, int64_t Hq,
+                                     int64_t Hkv, int64_t d, const uint8_t* k_packed, const uint8_t* k_scales,
+                                     const int32_t* k_pts, const uint8_t* vt_packed, const uint8_t* vt_scales,
+                                     const int32_t* v_pts, int causal, float tau, void* O, int64_t ldo, void* stream) {
+    FIREQ_NVTX("fireq_kv4q8_attention");
+    FIREQ_REQUIRE(q_fp8 && q_scale && k_packed && k_scales && k_pts && vt_packed && vt_scales && v_pts && O,
+                  FIREQ_ERROR_INVALID_VALUE, "fireq_kv4q8_attention: NULL required pointer");
+    FIREQ_REQUIRE(causal == 0 || causal == 1, FIREQ_ERROR_INVALID_VALUE, "fireq_kv4q8_attention: causal must be 0 or 1");
+    FIREQ_REQUIRE(tau > 0.0f, FIREQ_ERROR_INVALID_VALUE, "fireq_kv4q8_attention: tau must be positive");
+    FIREQ_REQUIRE(d == 128 && N >= 128 && N % 128 == 0 && N <= 65536 && B >= 1 && Hkv >= 1 && Hq >= Hkv &&
+                      Hq % Hkv == 0 && B * Hq * (N / 128) < (int64_t(1) << 31),
+                  FIREQ_ERROR_UNSUPPORTED_SHAPE,
+                  "fireq_kv4q8_attention: d must be 128, N a multiple of 128, Hq a multiple of Hkv");
+    FIREQ_REQUIRE(aligned16(q_fp8) && aligned16(k_packed) && aligned16(k_scales) && aligned16(vt_packed) &&
+                      aligned16(vt_scales) && aligned16(O) && ldo >= Hq * d && ldo % 8 == 0,
+                  FIREQ_ERROR_MISALIGNED, "fireq_kv4q8_attention: pointers must be 16-byte aligned, ldo >= Hq d, % 8");
+    return kv4q8_attention_impl(q_fp8, static_cast<const __nv_bfloat16*>(q_scale), k_packed, k_scales, k_pts,
+                                vt_packed, vt_scales, v_pts, B, N, Hq, Hkv, causal, tau,
+                                static_cast<__nv_bfloat16*>(O), ldo, static_cast<cudaStream_t>(stream));
 }
 
 // ------------------------------------------------------------ fused decode FFN

@@ -1,0 +1,372 @@
+// attention.cu -- fireq_kv4q8_attention: the paper's second kernel (section 3.2
+// P:178-291) on sm_100a: prefill self-attention with FP8 queries and an INT4 key / value cache
+// (KV4Q8-FP), the scores S = Q K^T and the output O = P V computed by the same INT4 x FP8
+// tensor-core path as the linear layers (LUT conversion of INT4 codes to FP8 by CUDA
+// cores; FP32 accumulation), the softmax quantized to FP8.
+//
+// One CTA per (sequence b, query head h, 128-query tile i); the causal tile i visits kv tiles
+// 0..i.  Warp roles:
+//   warps 0-3   converters: INT4 K / V^T blocks (layout v1, 8 KB + 128 FP8 scales per
+//               128 x 128 block) -> FP8 in shared memory, 128-byte swizzled K-major rows (the
+//               UMMA B operand), thread r <-> row r, 16-entry LUT per row
+//   warps 4-7   softmax + epilogue: thread r <-> query row r <-> TMEM lane r
+//   warp 8      TMA producer (Q tile once; packed K / V^T blocks into a 2-slot ring)
+//   warp 9      MMA issuer: S = Q K^T (A = Q in SMEM, B = K in SMEM, D = S in TMEM), then
+//               O += P V (A = P_hat in TMEM written by the softmax warps, B = V^T in SMEM)
+//   warp 10     TMEM allocator
+// Blackwell mapping of the paper's three-stage pipeline (Alg. 1): the scores of kv tile j are
+// computed while the softmax of tile j - 1 runs (two S buffers in TMEM) and O += P_{j-1} V_{j-1}
+// is issued after S_j -- wgmma_ss / softmax / wgmma_rs become tcgen05.mma (SMEM x SMEM) /
+// tcgen05.ld -> CUDA cores -> tcgen05.st / tcgen05.mma (TMEM x SMEM).  The softmax uses two
+// passes over the kv tiles (pass 1: exact row maxima; pass 2: P = exp(x - m), no rescaling of
+// O in TMEM), reading R36.  The value cache is stored transposed (V^T, groups of 128
+// tokens per channel), so the PV product needs no transposed load (P:236 transposes V in TMA).
+#include "common.cuh"
+#include "gemm_dev.cuh"
+#include "ptx.cuh"
+
+namespace fireq {
+using namespace dev;
+bool make_x_map(CUtensorMap* out, const uint8_t* x, int64_t M, int64_t K, int ntok);
+namespace {
+
+constexpr int kD = 128;                 // head dimension (one 128-group per K row)
+constexpr int kTile = 128;              // queries per CTA = kv per tile
+constexpr int kThreads = 11 * 32;
+
+struct AttnArgs {
+    const uint8_t* k_packed;            // [B][Hkv] x layout v1 [N][d]
+    const uint8_t* k_scales;
+    const uint8_t* vt_packed;           // [B][Hkv] x layout v1 [d][N]
+    const uint8_t* vt_scales;
+    const int32_t* k_pts;               // [B][Hkv][2] (fireq_quantize_kv pts_and_status of each head)
+    const int32_t* v_pts;
+    const __nv_bfloat16* q_scale;       // beta_q [B][Hq][N]
+    __nv_bfloat16* O;                   // [B * N][ldo], head h at columns [h d, h d + d)
+    int64_t ldo;
+    int N, Hq, Hkv, B, T;               // T = N / 128
+    int causal;
+    float tau_log2e;                    // softmax scale tau * log2(e)
+};
+
+// shared memory carve-up (offsets from a 1024-aligned base)
+constexpr int kOffQ = 0;                                 // Q tile, 16 KB, SW128
+constexpr int kOffCv = 16384;                            // 2 slots x {K 16 KB | V^T 16 KB}, SW128
+constexpr int kCvSlot = 32768;
+constexpr int kOffPk = kOffCv + 2 * kCvSlot;             // 2 slots x {K 8 KB | V 8 KB | sK 128 | sV 128}
+constexpr int kPkSlot = 16640;
+constexpr int kOffLut = kOffPk + 2 * kPkSlot;
+constexpr int kOffBar = kOffLut + 2048;
+constexpr int kNumBars = 18;
+constexpr int kOffMisc = kOffBar + kNumBars * 8;
+constexpr int kSmemBytes = kOffMisc + 64 + 1024;
+
+// TMEM columns
+constexpr uint32_t kTS = 0;             // S[2]: 128 columns each
+constexpr uint32_t kTO = 256;           // O: 128 columns
+constexpr uint32_t kTP = 384;           // P_hat[2]: 32 columns each (128 FP8 per lane)
+
+// One 128 x 128 block of layout v1 (row r's K-slice j at (j * 128 + r) * 16) -> FP8 row r of a
+// 128-byte-swizzled K-major tile (16-byte unit u of row r at (r >> 3) * 1024 + (r & 7) * 128 +
+// ((u ^ (r & 7)) * 16)): the mask-select converter, one LUT per row (the row's 128-group).
+__device__ __forceinline__ void convert_row(const uint8_t* packed, const uint8_t* sig, const uint4* lut,
+                                            uint8_t* dst, int r) {
+    const uint4 L = lut[sig[r] & 0x7F];
+    uint8_t* row = dst + (r >> 3) * 1024 + (r & 7) * 128;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint4 wv = *reinterpret_cast<const uint4*>(packed + (j * 128 + r) * 16);
+        uint4 o0, o1;
+        conv_mask_select(wv.x, L.x, L.y, L.z, L.w, o0.x, o0.y);
+        conv_mask_select(wv.y, L.x, L.y, L.z, L.w, o0.z, o0.w);
+        conv_mask_select(wv.z, L.x, L.y, L.z, L.w, o1.x, o1.y);
+        conv_mask_select(wv.w, L.x, L.y, L.z, L.w, o1.z, o1.w);
+        *reinterpret_cast<uint4*>(row + (((2 * j) ^ (r & 7)) * 16)) = o0;
+        *reinterpret_cast<uint4*>(row + (((2 * j + 1) ^ (r & 7)) * 16)) = o1;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ AttnArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* sQ = smem + kOffQ;
+    uint4* sLut = reinterpret_cast<uint4*>(smem + kOffLut);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
+    uint64_t* qfull = bars;
+    uint64_t* pk_full = bars + 1;       // [2]
+    uint64_t* pk_empty = bars + 3;      // [2]
+    uint64_t* cv_full = bars + 5;       // [2]
+    uint64_t* cv_empty = bars + 7;      // [2]
+    uint64_t* s_full = bars + 9;        // [2]
+    uint64_t* s_empty = bars + 11;      // [2]
+    uint64_t* p_full = bars + 13;       // [2]
+    uint64_t* pempty = bars + 15;       // [2] P_hat slot free (O MMAs that read it done)
+    uint64_t* ofull = bars + 17;        // O complete
+    uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kOffMisc);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // heavy (late) query tiles first: tile i of a causal head visits i + 1 kv tiles
+    const int per_tile = a.B * a.Hq;
+    const int i = a.T - 1 - (int)blockIdx.x / per_tile;
+    const int bh = (int)blockIdx.x % per_tile;
+    const int b = bh / a.Hq, h = bh % a.Hq;
+    const int hk = h / (a.Hq / a.Hkv);
+    const int nkv = a.causal ? i + 1 : a.T;
+    const int n_items = 2 * nkv;        // pass 1 (row maxima) then pass 2 (P, O)
+    const size_t kvh = (size_t)b * a.Hkv + hk;
+    const size_t blk = (size_t)a.N * kD / 2, sblk = (size_t)a.N * kD / 128;
+    const uint8_t* kp = a.k_packed + kvh * blk;
+    const uint8_t* ks = a.k_scales + kvh * sblk;
+    const uint8_t* vp = a.vt_packed + kvh * blk;
+    const uint8_t* vs = a.vt_scales + kvh * sblk;
+
+    // ------------------------------------------------------------ setup
+    if (warp == 8 && lane == 0) {
+        ptx::mbar_init(qfull, 1);
+        for (int s = 0; s < 2; ++s) {
+            ptx::mbar_init(&pk_full[s], 1);
+            ptx::mbar_init(&pk_empty[s], 4);
+            ptx::mbar_init(&cv_full[s], 4);
+            ptx::mbar_init(&cv_empty[s], 1);
+            ptx::mbar_init(&s_full[s], 1);
+            ptx::mbar_init(&s_empty[s], 4);
+            ptx::mbar_init(&p_full[s], 4);
+            ptx::mbar_init(&pempty[s], 1);
+        }
+        ptx::mbar_init(ofull, 1);
+        ptx::fence_mbar_init();
+        ptx::prefetch_tmap(&tmap_q);
+    }
+    if (warp == 10) {
+        ptx::tmem_alloc(&misc[0], 512);
+        ptx::tmem_relinquish();
+    }
+    build_lut(reinterpret_cast<uint8_t*>(sLut), threadIdx.x, kThreads);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = misc[0];
+
+    if (warp == 8) {
+        // ------------------------------------------------------- producer
+        ptx::pdl_wait();                     // Q, beta_q and the caches come from earlier kernels
+        const uint64_t pol = ptx::policy_evict_last();    // K / V blocks are re-read by the Hq / Hkv heads
+        if (ptx::elect_one()) {
+            ptx::mbar_arrive_expect_tx(qfull, kTile * kD);
+            ptx::tma_2d_g2s(sQ, &tmap_q, 0, ((b * a.Hq + h) * a.N) + i * kTile, qfull, ptx::policy_evict_first());
+        }
+        __syncwarp();
+        for (int t = 0; t < n_items; ++t) {
+            const int s = t & 1, ph = (t >> 1) & 1;
+            const bool p2 = t >= nkv;
+            const int j = p2 ? t - nkv : t;
+            ptx::mbar_wait(&pk_empty[s], ph ^ 1);
+            if (ptx::elect_one()) {
+                uint8_t* dst = smem + kOffPk + s * kPkSlot;
+                ptx::mbar_arrive_expect_tx(&pk_full[s], p2 ? 2 * (8192 + 128) : 8192 + 128);
+                ptx::bulk_g2s(dst, kp + (size_t)j * 8192, 8192, &pk_full[s], pol);
+                ptx::bulk_g2s(dst + 16384, ks + (size_t)j * 128, 128, &pk_full[s], pol);
+                if (p2) {
+                    ptx::bulk_g2s(dst + 8192, vp + (size_t)j * 8192, 8192, &pk_full[s], pol);
+                    ptx::bulk_g2s(dst + 16384 + 128, vs + (size_t)j * 128, 128, &pk_full[s], pol);
+                }
+            }
+            __syncwarp();
+        }
+    } else if (warp < 4) {
+        // ------------------------------------------------------- converters
+        const int r = threadIdx.x;
+        for (int t = 0; t < n_items; ++t) {
+            const int s = t & 1, ph = (t >> 1) & 1;
+            const bool p2 = t >= nkv;
+            ptx::mbar_wait(&pk_full[s], ph);
+            ptx::mbar_wait(&cv_empty[s], ph ^ 1);
+            const uint8_t* src = smem + kOffPk + s * kPkSlot;
+            uint8_t* cv = smem + kOffCv + s * kCvSlot;
+            convert_row(src, src + 16384, sLut, cv, r);
+            if (p2) convert_row(src + 8192, src + 16384 + 128, sLut, cv + 16384, r);
+            ptx::fence_proxy_async_smem();   // generic-proxy stores -> the MMA's async-proxy reads
+            __syncwarp();
+            if (lane == 0) {
+                ptx::mbar_arrive(&cv_full[s]);
+                ptx::mbar_arrive(&pk_empty[s]);
+            }
+        }
+    } else if (warp == 9) {
+        // ------------------------------------------------------- MMA issuer
+        constexpr uint32_t idesc = make_idesc(kTile, false);   // M = 128, N = 128, E4M3 x E4M3 -> F32
+        ptx::mbar_wait(qfull, 0);
+        ptx::tc_fence_after();
+        const uint64_t qdesc = smem_desc_sw128(ptx::smem_u32(sQ));
+        // O += P_hat(tp) V^T(tp).  The P_hat ring is indexed by the pass-2 item k2 = tp - nkv (only
+        // pass-2 items have one); the converted-tile ring by the global item tp.
+        auto issue_o = [&](int tp) {
+            const int k2 = tp - nkv, sp = k2 & 1, php = (k2 >> 1) & 1, sc = tp & 1;
+            ptx::mbar_wait(&p_full[sp], php);
+            ptx::tc_fence_after();
+            if (ptx::elect_one()) {
+                const uint64_t vdesc = smem_desc_sw128(ptx::smem_u32(smem + kOffCv + sc * kCvSlot + 16384));
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    ptx::mma_f8f6f4_ts(tmem + kTO, tmem + kTP + sp * 32 + k * 8, vdesc + (uint64_t)(k * 2), idesc,
+                                       (k2 > 0 || k > 0) ? 1u : 0u);
+                ptx::mma_commit(&pempty[sp]);
+                ptx::mma_commit(&cv_empty[sc]);
+            }
+            __syncwarp();
+        };
+        for (int t = 0; t < n_items; ++t) {
+            const int s = t & 1, ph = (t >> 1) & 1;
+            const bool p2 = t >= nkv;
+            ptx::mbar_wait(&cv_full[s], ph);
+            ptx::mbar_wait(&s_empty[s], ph ^ 1);
+            ptx::tc_fence_after();
+            if (ptx::elect_one()) {
+                const uint64_t kdesc = smem_desc_sw128(ptx::smem_u32(smem + kOffCv + s * kCvSlot));
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    ptx::mma_f8f6f4_ss(tmem + kTS + s * 128, qdesc + (uint64_t)(k * 2), kdesc + (uint64_t)(k * 2), idesc,
+                                       k > 0 ? 1u : 0u);
+                ptx::mma_commit(&s_full[s]);
+                if (!p2) ptx::mma_commit(&cv_empty[s]);
+            }
+            __syncwarp();
+            if (p2 && t > nkv) issue_o(t - 1);
+        }
+        issue_o(n_items - 1);
+        if (ptx::elect_one()) ptx::mma_commit(ofull);
+        __syncwarp();
+    } else if (warp >= 4 && warp < 8) {
+        // ------------------------------------------------------- softmax + epilogue
+        const int r = threadIdx.x - 128;                   // query row == TMEM lane
+        const uint32_t lane_base = (uint32_t)(r & ~31) << 16;
+        const int q = i * kTile + r;
+        const float bq = __bfloat162float(a.q_scale[((size_t)b * a.Hq + h) * a.N + q]);
+        const int nk = a.k_pts[2 * kvh], nv = a.v_pts[2 * kvh];
+        const float sc = bq * exp2_neg(nk) * a.tau_log2e;  // acc -> log2-domain logit
+        float m2 = -INFINITY, l = 0.0f;
+        for (int t = 0; t < n_items; ++t) {
+            const int s = t & 1, ph = (t >> 1) & 1;
+            const bool p2 = t >= nkv;
+            const int j = p2 ? t - nkv : t;
+            const bool diag = a.causal && j == i;
+            ptx::mbar_wait(&s_full[s], ph);
+            ptx::tc_fence_after();
+            const uint32_t ts = tmem + lane_base + kTS + s * 128;
+            if (!p2) {
+                float mx = -INFINITY;
+#pragma unroll 1
+                for (int c0 = 0; c0 < kTile; c0 += 16) {
+                    uint32_t v[16];
+                    ptx::tmem_ld_x16(ts + c0, v);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < 16; ++c)
+                        if (!diag || c0 + c <= r) mx = fmaxf(mx, __uint_as_float(v[c]) * sc);
+                }
+                m2 = fmaxf(m2, mx);
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&s_empty[s]);
+            } else {
+                const int k2 = t - nkv, sp = k2 & 1;
+                ptx::mbar_wait(&pempty[sp], ((k2 >> 1) & 1) ^ 1);   // O MMA of pass-2 item k2 - 2 read this slot
+                ptx::tc_fence_after();
+                const uint32_t tp = tmem + lane_base + kTP + sp * 32;
+#pragma unroll 1
+                for (int c0 = 0; c0 < kTile; c0 += 32) {
+                    uint32_t v[16], w8[8];
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        ptx::tmem_ld_x16(ts + c0 + hh * 16, v);
+                        ptx::tmem_wait_ld();
+                        float p[16];
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) {
+                            const bool keep = !diag || c0 + hh * 16 + c <= r;
+                            p[c] = keep ? exp2f(__uint_as_float(v[c]) * sc - m2) : 0.0f;
+                            l += p[c];
+                        }
+#pragma unroll
+                        for (int w = 0; w < 4; ++w)      // P_hat = E4M3_RN(448 P)
+                            w8[hh * 4 + w] = e4m3x2_rn(448.0f * p[4 * w], 448.0f * p[4 * w + 1]) |
+                                             (e4m3x2_rn(448.0f * p[4 * w + 2], 448.0f * p[4 * w + 3]) << 16);
+                    }
+                    ptx::tmem_st_x8(tp + c0 / 4, w8);
+                }
+                ptx::tmem_wait_st();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::mbar_arrive(&s_empty[s]);
+                    ptx::mbar_arrive(&p_full[sp]);
+                }
+            }
+        }
+        // epilogue: O = acc * 2^-n_v / 448 / l -> BF16, token-major [B N][ldo] at head h's columns
+        ptx::mbar_wait(ofull, 0);
+        ptx::tc_fence_after();
+        const float f = exp2_neg(nv) * (1.0f / 448.0f) / l;
+        __nv_bfloat16* orow = a.O + ((size_t)b * a.N + q) * a.ldo + (size_t)h * kD;
+#pragma unroll 1
+        for (int c0 = 0; c0 < kD; c0 += 16) {
+            uint32_t v[16];
+            ptx::tmem_ld_x16(tmem + lane_base + kTO + c0, v);
+            ptx::tmem_wait_ld();
+            __align__(16) __nv_bfloat16 y[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) y[c] = __float2bfloat16_rn(__uint_as_float(v[c]) * f);
+            reinterpret_cast<uint4*>(orow + c0)[0] = reinterpret_cast<const uint4*>(y)[0];
+            reinterpret_cast<uint4*>(orow + c0)[1] = reinterpret_cast<const uint4*>(y)[1];
+        }
+    }
+    // ------------------------------------------------------------ teardown
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (warp == 10) ptx::tmem_dealloc(tmem, 512);
+}
+
+}  // namespace
+
+fireq_status_t kv4q8_attention_impl(const uint8_t* q_fp8, const __nv_bfloat16* q_scale, const uint8_t* k_packed,
+                                    const uint8_t* k_scales, const int32_t* k_pts, const uint8_t* vt_packed,
+                                    const uint8_t* vt_scales, const int32_t* v_pts, int64_t B, int64_t N,
+                                    int64_t Hq, int64_t Hkv, int causal, float tau, __nv_bfloat16* O, int64_t ldo,
+                                    cudaStream_t stream) {
+    CUtensorMap map;
+    if (!make_x_map(&map, q_fp8, B * Hq * N, kD, kTile)) return fail(FIREQ_ERROR_CUDA, "cuTensorMapEncodeTiled failed");
+    AttnArgs args{};
+    args.k_packed = k_packed;
+    args.k_scales = k_scales;
+    args.vt_packed = vt_packed;
+    args.vt_scales = vt_scales;
+    args.k_pts = k_pts;
+    args.v_pts = v_pts;
+    args.q_scale = q_scale;
+    args.O = O;
+    args.ldo = ldo;
+    args.N = (int)N;
+    args.Hq = (int)Hq;
+    args.Hkv = (int)Hkv;
+    args.B = (int)B;
+    args.T = (int)(N / kTile);
+    args.causal = causal;
+    args.tau_log2e = tau * 1.4426950408889634f;
+    static bool attr_done[kMaxDevices] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
+        return fail(FIREQ_ERROR_CUDA, "cudaGetDevice failed");
+    if (!attr_done[dev]) {
+        if (cudaFuncSetAttribute(k_kv4q8_attn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) != cudaSuccess)
+            return fail(FIREQ_ERROR_CUDA, "cudaFuncSetAttribute(smem) failed");
+        attr_done[dev] = true;
+    }
+    const cudaError_t e = launch_ex(k_kv4q8_attn, dim3((unsigned)(B * Hq * args.T)), dim3(kThreads), kSmemBytes,
+                                    stream, 1u, false, map, args);
+    if (e != cudaSuccess) return fail(FIREQ_ERROR_CUDA, std::string("fireq_kv4q8_attention launch: ") + cudaGetErrorString(e));
+    return check_launch("fireq_kv4q8_attention");
+}
+
+}  // namespace fireq

@@ -63,9 +63,11 @@ __global__ void k_cas_finalize(const float* __restrict__ absmean, int64_t K, int
         if (cas_mode == 1) {
             const float a = absmean[k];
             lam = a > 0.0f ? __double2float_rn(__ddiv_rn((double)omega_s, (double)a)) : 1.0f;
+        } else if (cas_mode == 2) {
+            lam = lam_out ? lam_out[k] : 1.0f;     // caller-given multiplier (KV cache: 1 / t, CRS)
         }
         lam_ws[k] = lam;
-        if (lam_out) lam_out[k] = lam;
+        if (lam_out && cas_mode != 2) lam_out[k] = lam;
         if (c_out) c_out[k] = __float2bfloat16_rn(__fdiv_rn(1.0f, lam));
     }
 }

@@ -6,6 +6,7 @@ status codes to exceptions.  There is no CPU or PyTorch fallback: if the library
 is missing, or a tensor is not on a CUDA device, the call raises.
 """
 import ctypes
+import math
 import os
 
 import torch
@@ -81,6 +82,8 @@ def load(path=LIB_PATH):
         "fireq_ffn_w4a8_decode": ([P, I64, P, I64, I64, I64, P, P, I32, P, P, P, I32, P, I64, P, P, I64, P, SZ, P, SZ,
                                    P, SZ, P], C),
         "fireq_w4a8_gemm_residual": ([P, P, I64, I64, P, P, I64, I32, P, P, I64, P, I64, P, SZ, P], C),
+        "fireq_quantize_kv": ([P, I64, I64, P, P, P, P, P, SZ, P], C),
+        "fireq_kv4q8_attention": ([P, P, I64, I64, I64, I64, I64, P, P, P, P, P, P, C, ctypes.c_float, P, I64, P], C),
     }
     for name, (args, res) in sig.items():
         if os.environ.get("FIREQ_LOAD_PARTIAL") and not hasattr(lib, name):   # bisecting older builds
@@ -468,4 +471,54 @@ def w4a8_gemm_bf16s(xq, beta, packed, scales_bf16, N, pts_n, out=None, workspace
         out = torch.empty((M, N), dtype=torch.bfloat16, device=xq.device)
     _check(L.fireq_w4a8_gemm_bf16s(_ptr(xq), _ptr(beta), M, K, _ptr(packed), _ptr(scales_bf16), N, pts_n, _ptr(out),
                                    out.stride(0), _ptr(ws), ws.numel(), _stream(stream)), "fireq_w4a8_gemm_bf16s")
+    return out
+
+
+# ------------------------------------------------------------------ KV4Q8 attention (f4)
+class KVCache:
+    """INT4 keys and values of B sequences x Hkv heads (fireq_quantize_kv per head).
+
+    k_packed / k_scales: uint8 [B*Hkv][N*d/2] / [B*Hkv][N*d/128] (layout v1 of K_post [N][d]);
+    vt_packed / vt_scales: the same for V^T [d][N]; k_pts / v_pts: int32 [B*Hkv][2] {n, status}.
+    """
+
+    def __init__(self, K, V, chan_lambda=None, stream=None):
+        """K, V: bf16 [B][Hkv][N][d] (K post-RoPE); chan_lambda: fp32 [B*Hkv][d] or [Hkv][d] or None."""
+        B, Hkv, N, d = K.shape
+        dev = K.device
+        self.B, self.Hkv, self.N, self.d = B, Hkv, N, d
+        H = B * Hkv
+        self.k_packed = torch.empty((H, N * d // 2), dtype=torch.uint8, device=dev)
+        self.k_scales = torch.empty((H, N * d // 128), dtype=torch.uint8, device=dev)
+        self.vt_packed = torch.empty_like(self.k_packed)
+        self.vt_scales = torch.empty_like(self.k_scales)
+        self.k_pts = torch.zeros((H, 2), dtype=torch.int32, device=dev)
+        self.v_pts = torch.zeros((H, 2), dtype=torch.int32, device=dev)
+        L = lib()
+        need = max(L.fireq_quantize_weight_workspace_bytes(N, d), L.fireq_quantize_weight_workspace_bytes(d, N))
+        ws = torch.zeros(need, dtype=torch.uint8, device=dev)
+        Kc = K.reshape(H, N, d).contiguous()
+        Vt = V.reshape(H, N, d).transpose(1, 2).contiguous()          # [H][d][N]
+        for x in range(H):
+            lam = None
+            if chan_lambda is not None:
+                lam = chan_lambda[x] if chan_lambda.shape[0] == H else chan_lambda[x % Hkv]
+                lam = lam.contiguous()
+            _check(L.fireq_quantize_kv(_ptr(Kc[x]), N, d, _ptr(lam), _ptr(self.k_packed[x]), _ptr(self.k_scales[x]),
+                                       _ptr(self.k_pts[x]), _ptr(ws), ws.numel(), _stream(stream)), "fireq_quantize_kv")
+            _check(L.fireq_quantize_kv(_ptr(Vt[x]), d, N, None, _ptr(self.vt_packed[x]), _ptr(self.vt_scales[x]),
+                                       _ptr(self.v_pts[x]), _ptr(ws), ws.numel(), _stream(stream)), "fireq_quantize_kv")
+
+
+def kv4q8_attention(q_fp8, q_scale, cache, Hq, causal=True, tau=None, out=None, stream=None):
+    """O = fireq_kv4q8_attention(...): q_fp8 uint8 [B][Hq][N][d], q_scale bf16 [B][Hq][N] ->
+    bf16 [B*N][Hq*d] (token-major)."""
+    B, N, d = cache.B, cache.N, cache.d
+    if out is None:
+        out = torch.empty((B * N, Hq * d), dtype=torch.bfloat16, device=q_fp8.device)
+    tau = 1.0 / math.sqrt(d) if tau is None else tau
+    _check(lib().fireq_kv4q8_attention(_ptr(q_fp8), _ptr(q_scale), B, N, Hq, cache.Hkv, d, _ptr(cache.k_packed),
+                                       _ptr(cache.k_scales), _ptr(cache.k_pts), _ptr(cache.vt_packed),
+                                       _ptr(cache.vt_scales), _ptr(cache.v_pts), 1 if causal else 0, tau, _ptr(out),
+                                       out.stride(0), _stream(stream)), "fireq_kv4q8_attention")
     return out

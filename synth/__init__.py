@@ -79,3 +79,18 @@ def activations(M, K, seed):
 
 def layer_seed(config_idx, layer_idx):
     return SEED_BASE + 100 * config_idx + layer_idx
+
+
+def attention(B, N, Hq, Hkv, seed, d=128):
+    """Post-RoPE query / key / value heads of a Llama-style attention layer (bf16 bits):
+    Q [B][Hq][N][d] ~ N(0, 1); K [B][Hkv][N][d] ~ N(0, 1) with 2 outlier channels per kv head
+    (x16, the key outliers CRS targets) and their RoPE pair channels (x4); V ~ N(0, 1)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    q = rng.standard_normal((B, Hq, N, d), dtype=np.float32)
+    k = rng.standard_normal((B, Hkv, N, d), dtype=np.float32)
+    v = rng.standard_normal((B, Hkv, N, d), dtype=np.float32)
+    for hk in range(Hkv):
+        for c in rng.choice(d // 2, size=2, replace=False):
+            k[:, hk, :, c] *= 16.0
+            k[:, hk, :, c + d // 2] *= 4.0
+    return to_bf16_bits(q), to_bf16_bits(k), to_bf16_bits(v)
