@@ -23,10 +23,12 @@ as the linear layers.  Readings (R30-R37):
   Q           per (token, head) row: A1-A3 (beta_q bf16, E4M3 codes).
   scores      S = G2(Q_hat, K) (LUT re-rounding, fp64 sum), x = tau * S with tau = 1/sqrt(d),
               causal mask (kv > q -> excluded).
-  softmax     m = rowmax x, P = exp(x - m), l = rowsum P (fp64 here; the GPU in fp32).
-  P_hat       E4M3_RN(448 * P): P in (0, 1], so beta_P = 1/448 uses the full FP8 range
-              (the paper quantizes the softmax to FP8).
-  output      O = G2(P_hat, V^T) * (1/448) / l, BF16 at the end.
+  softmax     Alg. 1 with B_c = 128 kv per tile: running max m_i, s_i =
+              exp(m_old - m_new), P_ij = exp(x_ij - m_new), l_i = s_i l_i + rowsum(P_ij)
+              (fp64 here; the GPU in fp32).
+  P_hat       E4M3_RN(448 * P_ij) per tile: P in (0, 1], so beta_P = 1/448 uses the full FP8
+              range (the softmax quantized to FP8).
+  output      O_i = s_i O_i + G2(P_hat_ij, V_j^T) per tile; O = O_i 2^-n_v / 448 / l_i, BF16.
 """
 import numpy as np
 
@@ -84,8 +86,10 @@ class KV4Head:
         self.vt_deq = gemm.dequantize_weight(self.vt.packed, self.vt.scales, d, N)
 
 
-def attention_head(Q, kv, t=None, causal=True, tau=None):
-    """One query head against one KV4 head.  Q [N][d] bf16 values (post-RoPE).
+def attention_head(Q, kv, t=None, causal=True, tau=None, bc=128):
+    """One query head against one KV4 head, Alg. 1 step by step with B_c = bc:
+    running row max m, P_j = exp(x_j - m_new) quantized to FP8 per kv tile, O = s * O + P_hat_j V_j,
+    l = s * l + rowsum(P_j), s = exp(m_old - m_new).  Q [N][d] bf16 values (post-RoPE).
     Returns (O bf16 values [N][d], O fp64 before the BF16 rounding, dict of intermediates)."""
     Q = np.asarray(Q, dtype=np.float64)
     N, d = Q.shape
@@ -96,13 +100,24 @@ def attention_head(Q, kv, t=None, causal=True, tau=None):
     x = tau * S
     if causal:
         x = np.where(np.arange(N)[None, :] <= np.arange(N)[:, None], x, -np.inf)
-    m = x.max(axis=1, keepdims=True)
-    P = np.exp(x - m)
-    l = P.sum(axis=1)
-    p_codes = e4m3_encode(e4m3_rn(448.0 * P))                                # FP8 softmax
-    beta_p = np.full(N, 1.0 / 448.0)
-    O = gemm.gemm_reference(p_codes, beta_p, None, None, d, N, kv.vt.n, w_deq=kv.vt_deq) / l[:, None]
-    return bf16_rn(O), O, dict(q_codes=q_codes, beta_q=beta_q, S=S, m=m[:, 0], l=l, p_codes=p_codes)
+    m = np.full(N, -np.inf)
+    l = np.zeros(N)
+    O = np.zeros((N, d))
+    p_codes = np.zeros((N, N), dtype=np.uint8)
+    with np.errstate(invalid="ignore"):
+        for j0 in range(0, N, bc):
+            xj = x[:, j0:j0 + bc]
+            m_new = np.maximum(m, xj.max(axis=1))
+            s = np.where(m_new == m, 1.0, np.exp(m - m_new))                 # exp(-inf) = 0 on tile 0
+            Pj = np.exp(xj - m_new[:, None])
+            l = s * l + Pj.sum(axis=1)
+            pc = e4m3_encode(e4m3_rn(448.0 * Pj))                            # FP8 softmax tile
+            p_codes[:, j0:j0 + bc] = pc
+            O = s[:, None] * O + gemm.gemm_reference(pc, np.ones(N), None, None, d, bc, 0,
+                                                     w_deq=kv.vt_deq[:, j0:j0 + bc])
+            m = m_new
+    O = O * 2.0 ** (-kv.vt.n) / 448.0 / l[:, None]
+    return bf16_rn(O), O, dict(q_codes=q_codes, beta_q=beta_q, S=S, m=m, l=l, p_codes=p_codes)
 
 
 def attention_unquantized(Q, K, V, causal=True, tau=None):

@@ -6,10 +6,11 @@
 //
 // One CTA per (sequence b, query head h, 128-query tile i); the causal tile i visits kv tiles
 // 0..i.  Warp roles:
-//   warps 0-3   converters: INT4 K / V^T blocks (layout v1, 8 KB + 128 FP8 scales per
+//   warps 0-3   key converters, warps 11-14 value converters: INT4 K / V^T blocks (layout v1, 8 KB + 128 FP8 scales per
 //               128 x 128 block) -> FP8 in shared memory, 128-byte swizzled K-major rows (the
 //               UMMA B operand), thread r <-> row r, 16-entry LUT per row
-//   warps 4-7   softmax + epilogue: thread r <-> query row r <-> TMEM lane r
+//   warps 4-7, 15-18   softmax + epilogue, two halves of the kv / d columns: thread r <-> query
+//               row r <-> TMEM lane r
 //   warp 8      TMA producer (Q tile once; packed K / V^T blocks into a 2-slot ring)
 //   warp 9      MMA issuer: S = Q K^T (A = Q in SMEM, B = K in SMEM, D = S in TMEM), then
 //               O += P V (A = P_hat in TMEM written by the softmax warps, B = V^T in SMEM)
@@ -17,9 +18,9 @@
 // Blackwell mapping of the paper's three-stage pipeline (Alg. 1): the scores of kv tile j are
 // computed while the softmax of tile j - 1 runs (two S buffers in TMEM) and O += P_{j-1} V_{j-1}
 // is issued after S_j -- wgmma_ss / softmax / wgmma_rs become tcgen05.mma (SMEM x SMEM) /
-// tcgen05.ld -> CUDA cores -> tcgen05.st / tcgen05.mma (TMEM x SMEM).  The softmax uses two
-// passes over the kv tiles (pass 1: exact row maxima; pass 2: P = exp(x - m), no rescaling of
-// O in TMEM), reading R36.  The value cache is stored transposed (V^T, groups of 128
+// tcgen05.ld -> CUDA cores -> tcgen05.st / tcgen05.mma (TMEM x SMEM).  The softmax is Alg. 1's
+// online softmax with B_c = 128: running row max m, P_j = exp(x_j - m) quantized to FP8 per
+// tile, O rescaled by exp(m_old - m_new) in TMEM before O += P_j V_j (line 14).  The value cache is stored transposed (V^T, groups of 128
 // tokens per channel), so the PV product needs no transposed load (P:236 transposes V in TMA).
 #include "common.cuh"
 #include "gemm_dev.cuh"
@@ -32,7 +33,7 @@ namespace {
 
 constexpr int kD = 128;                 // head dimension (one 128-group per K row)
 constexpr int kTile = 128;              // queries per CTA = kv per tile
-constexpr int kThreads = 11 * 32;
+constexpr int kThreads = 19 * 32;    // + warps 11-14 value converters, 15-18 second softmax half
 
 struct AttnArgs {
     const uint8_t* k_packed;            // [B][Hkv] x layout v1 [N][d]
@@ -51,20 +52,28 @@ struct AttnArgs {
 
 // shared memory carve-up (offsets from a 1024-aligned base)
 constexpr int kOffQ = 0;                                 // Q tile, 16 KB, SW128
-constexpr int kOffCv = 16384;                            // 2 slots x {K 16 KB | V^T 16 KB}, SW128
-constexpr int kCvSlot = 32768;
-constexpr int kOffPk = kOffCv + 2 * kCvSlot;             // 2 slots x {K 8 KB | V 8 KB | sK 128 | sV 128}
+constexpr int kRing = 3;                                 // depth of the packed / converted K / V rings
+constexpr int kOffKc = 16384;                            // kRing x K tile 16 KB, SW128
+constexpr int kOffVc = kOffKc + kRing * 16384;           // kRing x V^T tile 16 KB, SW128
+constexpr int kOffPk = kOffVc + kRing * 16384;           // kRing x {K 8 KB | V 8 KB | sK 128 | sV 128}
 constexpr int kPkSlot = 16640;
-constexpr int kOffLut = kOffPk + 2 * kPkSlot;
+constexpr int kOffLut = kOffPk + kRing * kPkSlot;
 constexpr int kOffBar = kOffLut + 2048;
-constexpr int kNumBars = 18;
-constexpr int kOffMisc = kOffBar + kNumBars * 8;
+constexpr int kNumBars = 28;
+constexpr int kOffX = kOffBar + kNumBars * 8;              // softmax halves' row maxima [2][2][128] + l [2][128]
+constexpr int kOffMisc = kOffX + 6 * 128 * 4;
 constexpr int kSmemBytes = kOffMisc + 64 + 1024;
 
 // TMEM columns
 constexpr uint32_t kTS = 0;             // S[2]: 128 columns each
 constexpr uint32_t kTO = 256;           // O: 128 columns
 constexpr uint32_t kTP = 384;           // P_hat[2]: 32 columns each (128 FP8 per lane)
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
 // One 128 x 128 block of layout v1 (row r's K-slice j at (j * 128 + r) * 16) -> FP8 row r of a
 // 128-byte-swizzled K-major tile (16-byte unit u of row r at (r >> 3) * 1024 + (r & 7) * 128 +
@@ -94,15 +103,17 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
     uint4* sLut = reinterpret_cast<uint4*>(smem + kOffLut);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
     uint64_t* qfull = bars;
-    uint64_t* pk_full = bars + 1;       // [2]
-    uint64_t* pk_empty = bars + 3;      // [2]
-    uint64_t* cv_full = bars + 5;       // [2]
-    uint64_t* cv_empty = bars + 7;      // [2]
-    uint64_t* s_full = bars + 9;        // [2]
-    uint64_t* s_empty = bars + 11;      // [2]
-    uint64_t* p_full = bars + 13;       // [2]
-    uint64_t* pempty = bars + 15;       // [2] P_hat slot free (O MMAs that read it done)
-    uint64_t* ofull = bars + 17;        // O complete
+    uint64_t* pk_full = bars + 1;       // [kRing] packed K + V of tile j landed
+    uint64_t* pk_empty = bars + 4;      // [kRing] both converter warpgroups have read them
+    uint64_t* kc_full = bars + 7;       // [kRing] K_j converted (FP8, SMEM)
+    uint64_t* kc_empty = bars + 10;     // [kRing] S_j MMAs done reading it
+    uint64_t* vc_full = bars + 13;      // [kRing] V^T_j converted
+    uint64_t* vc_empty = bars + 16;     // [kRing] O_j MMAs done reading it
+    uint64_t* s_full = bars + 19;       // [2]
+    uint64_t* s_empty = bars + 21;      // [2]
+    uint64_t* p_full = bars + 23;       // [2]
+    uint64_t* pempty = bars + 25;       // [2] P_hat slot free (O MMAs that read it done)
+    uint64_t* ofull = bars + 27;        // O complete
     uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kOffMisc);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -113,7 +124,6 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
     const int b = bh / a.Hq, h = bh % a.Hq;
     const int hk = h / (a.Hq / a.Hkv);
     const int nkv = a.causal ? i + 1 : a.T;
-    const int n_items = 2 * nkv;        // pass 1 (row maxima) then pass 2 (P, O)
     const size_t kvh = (size_t)b * a.Hkv + hk;
     const size_t blk = (size_t)a.N * kD / 2, sblk = (size_t)a.N * kD / 128;
     const uint8_t* kp = a.k_packed + kvh * blk;
@@ -124,14 +134,18 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
     // ------------------------------------------------------------ setup
     if (warp == 8 && lane == 0) {
         ptx::mbar_init(qfull, 1);
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < kRing; ++s) {
             ptx::mbar_init(&pk_full[s], 1);
-            ptx::mbar_init(&pk_empty[s], 4);
-            ptx::mbar_init(&cv_full[s], 4);
-            ptx::mbar_init(&cv_empty[s], 1);
+            ptx::mbar_init(&pk_empty[s], 8);
+            ptx::mbar_init(&kc_full[s], 4);
+            ptx::mbar_init(&kc_empty[s], 1);
+            ptx::mbar_init(&vc_full[s], 4);
+            ptx::mbar_init(&vc_empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(&s_full[s], 1);
-            ptx::mbar_init(&s_empty[s], 4);
-            ptx::mbar_init(&p_full[s], 4);
+            ptx::mbar_init(&s_empty[s], 8);
+            ptx::mbar_init(&p_full[s], 8);
             ptx::mbar_init(&pempty[s], 1);
         }
         ptx::mbar_init(ofull, 1);
@@ -157,39 +171,36 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
             ptx::tma_2d_g2s(sQ, &tmap_q, 0, ((b * a.Hq + h) * a.N) + i * kTile, qfull, ptx::policy_evict_first());
         }
         __syncwarp();
-        for (int t = 0; t < n_items; ++t) {
-            const int s = t & 1, ph = (t >> 1) & 1;
-            const bool p2 = t >= nkv;
-            const int j = p2 ? t - nkv : t;
+        for (int j = 0; j < nkv; ++j) {
+            const int s = j % kRing, ph = (j / kRing) & 1;
             ptx::mbar_wait(&pk_empty[s], ph ^ 1);
             if (ptx::elect_one()) {
                 uint8_t* dst = smem + kOffPk + s * kPkSlot;
-                ptx::mbar_arrive_expect_tx(&pk_full[s], p2 ? 2 * (8192 + 128) : 8192 + 128);
+                ptx::mbar_arrive_expect_tx(&pk_full[s], 2 * (8192 + 128));
                 ptx::bulk_g2s(dst, kp + (size_t)j * 8192, 8192, &pk_full[s], pol);
                 ptx::bulk_g2s(dst + 16384, ks + (size_t)j * 128, 128, &pk_full[s], pol);
-                if (p2) {
-                    ptx::bulk_g2s(dst + 8192, vp + (size_t)j * 8192, 8192, &pk_full[s], pol);
-                    ptx::bulk_g2s(dst + 16384 + 128, vs + (size_t)j * 128, 128, &pk_full[s], pol);
-                }
+                ptx::bulk_g2s(dst + 8192, vp + (size_t)j * 8192, 8192, &pk_full[s], pol);
+                ptx::bulk_g2s(dst + 16384 + 128, vs + (size_t)j * 128, 128, &pk_full[s], pol);
             }
             __syncwarp();
         }
-    } else if (warp < 4) {
-        // ------------------------------------------------------- converters
-        const int r = threadIdx.x;
-        for (int t = 0; t < n_items; ++t) {
-            const int s = t & 1, ph = (t >> 1) & 1;
-            const bool p2 = t >= nkv;
+    } else if (warp < 4 || (warp >= 11 && warp < 15)) {
+        // ------------------------------------------------------- converters (warps 0-3: K, 11-14: V^T)
+        const bool vconv = warp >= 11;
+        const int r = vconv ? (int)threadIdx.x - 11 * 32 : (int)threadIdx.x;
+        uint64_t* c_full = vconv ? vc_full : kc_full;
+        uint64_t* c_empty = vconv ? vc_empty : kc_empty;
+        for (int j = 0; j < nkv; ++j) {
+            const int s = j % kRing, ph = (j / kRing) & 1;
             ptx::mbar_wait(&pk_full[s], ph);
-            ptx::mbar_wait(&cv_empty[s], ph ^ 1);
+            ptx::mbar_wait(&c_empty[s], ph ^ 1);
             const uint8_t* src = smem + kOffPk + s * kPkSlot;
-            uint8_t* cv = smem + kOffCv + s * kCvSlot;
-            convert_row(src, src + 16384, sLut, cv, r);
-            if (p2) convert_row(src + 8192, src + 16384 + 128, sLut, cv + 16384, r);
+            if (!vconv) convert_row(src, src + 16384, sLut, smem + kOffKc + s * 16384, r);
+            else convert_row(src + 8192, src + 16384 + 128, sLut, smem + kOffVc + s * 16384, r);
             ptx::fence_proxy_async_smem();   // generic-proxy stores -> the MMA's async-proxy reads
             __syncwarp();
             if (lane == 0) {
-                ptx::mbar_arrive(&cv_full[s]);
+                ptx::mbar_arrive(&c_full[s]);
                 ptx::mbar_arrive(&pk_empty[s]);
             }
         }
@@ -199,120 +210,148 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
         ptx::mbar_wait(qfull, 0);
         ptx::tc_fence_after();
         const uint64_t qdesc = smem_desc_sw128(ptx::smem_u32(sQ));
-        // O += P_hat(tp) V^T(tp).  The P_hat ring is indexed by the pass-2 item k2 = tp - nkv (only
-        // pass-2 items have one); the converted-tile ring by the global item tp.
-        auto issue_o = [&](int tp) {
-            const int k2 = tp - nkv, sp = k2 & 1, php = (k2 >> 1) & 1, sc = tp & 1;
-            ptx::mbar_wait(&p_full[sp], php);
+        // O += P_hat(j) V^T(j) once the softmax has written P_hat(j) and rescaled O (Alg. 1 line 14)
+        auto issue_o = [&](int j) {
+            const int s = j & 1, sv = j % kRing;
+            ptx::mbar_wait(&vc_full[sv], (j / kRing) & 1);
+            ptx::mbar_wait(&p_full[s], (j >> 1) & 1);
             ptx::tc_fence_after();
             if (ptx::elect_one()) {
-                const uint64_t vdesc = smem_desc_sw128(ptx::smem_u32(smem + kOffCv + sc * kCvSlot + 16384));
+                const uint64_t vdesc = smem_desc_sw128(ptx::smem_u32(smem + kOffVc + sv * 16384));
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                    ptx::mma_f8f6f4_ts(tmem + kTO, tmem + kTP + sp * 32 + k * 8, vdesc + (uint64_t)(k * 2), idesc,
-                                       (k2 > 0 || k > 0) ? 1u : 0u);
-                ptx::mma_commit(&pempty[sp]);
-                ptx::mma_commit(&cv_empty[sc]);
+                    ptx::mma_f8f6f4_ts(tmem + kTO, tmem + kTP + s * 32 + k * 8, vdesc + (uint64_t)(k * 2), idesc,
+                                       (j > 0 || k > 0) ? 1u : 0u);
+                ptx::mma_commit(&pempty[s]);
+                ptx::mma_commit(&vc_empty[sv]);
             }
             __syncwarp();
         };
-        for (int t = 0; t < n_items; ++t) {
-            const int s = t & 1, ph = (t >> 1) & 1;
-            const bool p2 = t >= nkv;
-            ptx::mbar_wait(&cv_full[s], ph);
+        for (int j = 0; j < nkv; ++j) {
+            const int s = j & 1, ph = (j >> 1) & 1, sk = j % kRing;
+            ptx::mbar_wait(&kc_full[sk], (j / kRing) & 1);
             ptx::mbar_wait(&s_empty[s], ph ^ 1);
             ptx::tc_fence_after();
-            if (ptx::elect_one()) {
-                const uint64_t kdesc = smem_desc_sw128(ptx::smem_u32(smem + kOffCv + s * kCvSlot));
+            if (ptx::elect_one()) {          // S_j = Q K_j^T (Alg. 1 line 12), before O += P_{j-1} V_{j-1}
+                const uint64_t kdesc = smem_desc_sw128(ptx::smem_u32(smem + kOffKc + sk * 16384));
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     ptx::mma_f8f6f4_ss(tmem + kTS + s * 128, qdesc + (uint64_t)(k * 2), kdesc + (uint64_t)(k * 2), idesc,
                                        k > 0 ? 1u : 0u);
                 ptx::mma_commit(&s_full[s]);
-                if (!p2) ptx::mma_commit(&cv_empty[s]);
+                ptx::mma_commit(&kc_empty[sk]);
             }
             __syncwarp();
-            if (p2 && t > nkv) issue_o(t - 1);
+            if (j > 0) issue_o(j - 1);
         }
-        issue_o(n_items - 1);
+        issue_o(nkv - 1);
         if (ptx::elect_one()) ptx::mma_commit(ofull);
         __syncwarp();
-    } else if (warp >= 4 && warp < 8) {
-        // ------------------------------------------------------- softmax + epilogue
-        const int r = threadIdx.x - 128;                   // query row == TMEM lane
+    } else if ((warp >= 4 && warp < 8) || warp >= 15) {
+        // ------------------------------------------------------- online softmax + epilogue (Alg. 1)
+        // Two warpgroups share the rows: half hf takes kv columns [64 hf, 64 hf + 64) of S, TMEM
+        // columns [16 hf, 16 hf + 16) of P_hat and d columns [64 hf, 64 hf + 64) of O; the row max
+        // of each tile is exchanged through shared memory (one named barrier per tile).
+        const int hf = warp >= 15 ? 1 : 0;
+        // query row == TMEM lane; a warp reaches only TMEM lanes [32 (warp % 4), + 32)
+        const int r = (warp & 3) * 32 + lane;
         const uint32_t lane_base = (uint32_t)(r & ~31) << 16;
+        float* xmax = reinterpret_cast<float*>(smem + kOffX);      // [tile parity][half][row]
+        float* xl = xmax + 4 * 128;                                // [half][row]
         const int q = i * kTile + r;
         const float bq = __bfloat162float(a.q_scale[((size_t)b * a.Hq + h) * a.N + q]);
         const int nk = a.k_pts[2 * kvh], nv = a.v_pts[2 * kvh];
-        const float sc = bq * exp2_neg(nk) * a.tau_log2e;  // acc -> log2-domain logit
-        float m2 = -INFINITY, l = 0.0f;
-        for (int t = 0; t < n_items; ++t) {
-            const int s = t & 1, ph = (t >> 1) & 1;
-            const bool p2 = t >= nkv;
-            const int j = p2 ? t - nkv : t;
+        const float sc = bq * exp2_neg(nk) * a.tau_log2e;  // acc -> log2-domain logit (sc > 0)
+        constexpr float kLog2_448 = 8.807354922057604f;    // 448 P = exp2(x - m + log2 448)
+        float m2 = -INFINITY, l = 0.0f;                    // l accumulates 448 P (this half's columns)
+        for (int j = 0; j < nkv; ++j) {
+            const int s = j & 1, ph = (j >> 1) & 1;
             const bool diag = a.causal && j == i;
             ptx::mbar_wait(&s_full[s], ph);
             ptx::tc_fence_after();
-            const uint32_t ts = tmem + lane_base + kTS + s * 128;
-            if (!p2) {
-                float mx = -INFINITY;
+            const uint32_t ts = tmem + lane_base + kTS + s * 128 + hf * 64;
+            // m_new = max(m_old, rowmax(x_j)) (lines 10-11), max over the raw accumulators (sc > 0)
+            float mx = -INFINITY;
 #pragma unroll 1
-                for (int c0 = 0; c0 < kTile; c0 += 16) {
-                    uint32_t v[16];
-                    ptx::tmem_ld_x16(ts + c0, v);
+            for (int c0 = 0; c0 < 64; c0 += 16) {
+                uint32_t v[16];
+                ptx::tmem_ld_x16(ts + c0, v);
+                ptx::tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < 16; ++c)
+                    if (!diag || hf * 64 + c0 + c <= r) mx = fmaxf(mx, __uint_as_float(v[c]));
+            }
+            xmax[(s * 2 + hf) * 128 + r] = mx;
+            ptx::named_bar_sync(3, 256);
+            mx = fmaxf(mx, xmax[(s * 2 + (hf ^ 1)) * 128 + r]);
+            const float mnew = fmaxf(m2, mx * sc);
+            const float resc = ex2_approx(m2 - mnew);        // s_i = exp(m_old - m_new); 0 on tile 0
+            m2 = mnew;
+            l *= resc;
+            const float off = mnew - kLog2_448;
+            // 448 P_j = exp2(x_j - m_new + log2 448), l += rowsum, P_hat_j = E4M3_RN(448 P_j) (line 13).
+            // The P slot was last read by the O MMA of tile j - 2, complete once O(j - 1) is.
+            if (j >= 1) ptx::mbar_wait(&pempty[(j - 1) & 1], ((j - 1) >> 1) & 1);
+            ptx::tc_fence_after();
+            const uint32_t tp = tmem + lane_base + kTP + s * 32 + hf * 16;
+#pragma unroll 1
+            for (int c0 = 0; c0 < 64; c0 += 32) {
+                uint32_t v[16], w8[8];
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    ptx::tmem_ld_x16(ts + c0 + hh * 16, v);
                     ptx::tmem_wait_ld();
+                    float p[16];
 #pragma unroll
-                    for (int c = 0; c < 16; ++c)
-                        if (!diag || c0 + c <= r) mx = fmaxf(mx, __uint_as_float(v[c]) * sc);
-                }
-                m2 = fmaxf(m2, mx);
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&s_empty[s]);
-            } else {
-                const int k2 = t - nkv, sp = k2 & 1;
-                ptx::mbar_wait(&pempty[sp], ((k2 >> 1) & 1) ^ 1);   // O MMA of pass-2 item k2 - 2 read this slot
-                ptx::tc_fence_after();
-                const uint32_t tp = tmem + lane_base + kTP + sp * 32;
-#pragma unroll 1
-                for (int c0 = 0; c0 < kTile; c0 += 32) {
-                    uint32_t v[16], w8[8];
-#pragma unroll
-                    for (int hh = 0; hh < 2; ++hh) {
-                        ptx::tmem_ld_x16(ts + c0 + hh * 16, v);
-                        ptx::tmem_wait_ld();
-                        float p[16];
-#pragma unroll
-                        for (int c = 0; c < 16; ++c) {
-                            const bool keep = !diag || c0 + hh * 16 + c <= r;
-                            p[c] = keep ? exp2f(__uint_as_float(v[c]) * sc - m2) : 0.0f;
-                            l += p[c];
-                        }
-#pragma unroll
-                        for (int w = 0; w < 4; ++w)      // P_hat = E4M3_RN(448 P)
-                            w8[hh * 4 + w] = e4m3x2_rn(448.0f * p[4 * w], 448.0f * p[4 * w + 1]) |
-                                             (e4m3x2_rn(448.0f * p[4 * w + 2], 448.0f * p[4 * w + 3]) << 16);
+                    for (int c = 0; c < 16; ++c) {
+                        const bool keep = !diag || hf * 64 + c0 + hh * 16 + c <= r;
+                        p[c] = keep ? ex2_approx(__fmaf_rn(__uint_as_float(v[c]), sc, -off)) : 0.0f;
+                        l += p[c];
                     }
-                    ptx::tmem_st_x8(tp + c0 / 4, w8);
+#pragma unroll
+                    for (int w = 0; w < 4; ++w)
+                        w8[hh * 4 + w] = e4m3x2_rn(p[4 * w], p[4 * w + 1]) | (e4m3x2_rn(p[4 * w + 2], p[4 * w + 3]) << 16);
                 }
-                ptx::tmem_wait_st();
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    ptx::mbar_arrive(&s_empty[s]);
-                    ptx::mbar_arrive(&p_full[sp]);
+                ptx::tmem_st_x8(tp + c0 / 4, w8);
+            }
+            // O = s_i * O (line 14) on this half's d columns: O holds tiles 0 .. j-1
+            if (j >= 1 && __any_sync(0xffffffffu, resc != 1.0f)) {
+#pragma unroll 1
+                for (int c0 = 0; c0 < 64; c0 += 16) {
+                    const uint32_t to = tmem + lane_base + kTO + hf * 64 + c0;
+                    uint32_t v[16];
+                    ptx::tmem_ld_x16(to, v);
+                    ptx::tmem_wait_ld();
+                    uint32_t lo[8], hi[8];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        lo[c] = __float_as_uint(__uint_as_float(v[c]) * resc);
+                        hi[c] = __float_as_uint(__uint_as_float(v[8 + c]) * resc);
+                    }
+                    ptx::tmem_st_x8(to, lo);
+                    ptx::tmem_st_x8(to + 8, hi);
                 }
             }
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                ptx::mbar_arrive(&s_empty[s]);
+                ptx::mbar_arrive(&p_full[s]);
+            }
         }
-        // epilogue: O = acc * 2^-n_v / 448 / l -> BF16, token-major [B N][ldo] at head h's columns
+        // epilogue: O = acc * 2^-n_v / (448 l) -> BF16, token-major [B N][ldo] at head h's columns
+        xl[hf * 128 + r] = l;
+        ptx::named_bar_sync(3, 256);
+        const float ltot = xl[r] + xl[128 + r];
         ptx::mbar_wait(ofull, 0);
         ptx::tc_fence_after();
-        const float f = exp2_neg(nv) * (1.0f / 448.0f) / l;
-        __nv_bfloat16* orow = a.O + ((size_t)b * a.N + q) * a.ldo + (size_t)h * kD;
+        const float f = exp2_neg(nv) / ltot;
+        __nv_bfloat16* orow = a.O + ((size_t)b * a.N + q) * a.ldo + (size_t)h * kD + hf * 64;
 #pragma unroll 1
-        for (int c0 = 0; c0 < kD; c0 += 16) {
+        for (int c0 = 0; c0 < 64; c0 += 16) {
             uint32_t v[16];
-            ptx::tmem_ld_x16(tmem + lane_base + kTO + c0, v);
+            ptx::tmem_ld_x16(tmem + lane_base + kTO + hf * 64 + c0, v);
             ptx::tmem_wait_ld();
             __align__(16) __nv_bfloat16 y[16];
 #pragma unroll
