@@ -271,15 +271,28 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
             ptx::tc_fence_after();
             const uint32_t ts = tmem + lane_base + kTS + s * 128 + hf * 64;
             // m_new = max(m_old, rowmax(x_j)) (lines 10-11), max over the raw accumulators (sc > 0)
+            // (the causal mask matters on the diagonal tile only: a separate loop keeps the
+            // per-element selects out of the others)
             float mx = -INFINITY;
+            if (!diag) {
 #pragma unroll 1
-            for (int c0 = 0; c0 < 64; c0 += 16) {
-                uint32_t v[16];
-                ptx::tmem_ld_x16(ts + c0, v);
-                ptx::tmem_wait_ld();
+                for (int c0 = 0; c0 < 64; c0 += 16) {
+                    uint32_t v[16];
+                    ptx::tmem_ld_x16(ts + c0, v);
+                    ptx::tmem_wait_ld();
 #pragma unroll
-                for (int c = 0; c < 16; ++c)
-                    if (!diag || hf * 64 + c0 + c <= r) mx = fmaxf(mx, __uint_as_float(v[c]));
+                    for (int c = 0; c < 16; ++c) mx = fmaxf(mx, __uint_as_float(v[c]));
+                }
+            } else {
+#pragma unroll 1
+                for (int c0 = 0; c0 < 64; c0 += 16) {
+                    uint32_t v[16];
+                    ptx::tmem_ld_x16(ts + c0, v);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < 16; ++c)
+                        if (hf * 64 + c0 + c <= r) mx = fmaxf(mx, __uint_as_float(v[c]));
+                }
             }
             xmax[(s * 2 + hf) * 128 + r] = mx;
             ptx::named_bar_sync(3, 256);
@@ -303,11 +316,14 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
                     ptx::tmem_wait_ld();
                     float p[16];
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) {
-                        const bool keep = !diag || hf * 64 + c0 + hh * 16 + c <= r;
-                        p[c] = keep ? ex2_approx(__fmaf_rn(__uint_as_float(v[c]), sc, -off)) : 0.0f;
-                        l += p[c];
+                    for (int c = 0; c < 16; ++c) p[c] = ex2_approx(__fmaf_rn(__uint_as_float(v[c]), sc, -off));
+                    if (diag) {
+#pragma unroll
+                        for (int c = 0; c < 16; ++c)
+                            if (hf * 64 + c0 + hh * 16 + c > r) p[c] = 0.0f;
                     }
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) l += p[c];
 #pragma unroll
                     for (int w = 0; w < 4; ++w)
                         w8[hh * 4 + w] = e4m3x2_rn(p[4 * w], p[4 * w + 1]) | (e4m3x2_rn(p[4 * w + 2], p[4 * w + 3]) << 16);
