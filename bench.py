@@ -517,6 +517,7 @@ def run_fireq(args, rank, world, dev):
     # BASELINE configs[3] at P = 1 (the column-parallel runs report P = 2/4/8)
     from paper_2505_20839_b200.c4 import c4_figures
     c4_info = c4_figures(F, dev, stream, 0, 1, comm=None) if not args.no_c4 else None
+    attn_info = attention_figures(F, dev, stream, peaks) if not args.no_attention else None
 
     # ---------------- cpu baseline (oracle on a bounded sample)
     cpu = cpu_oracle_baseline() if not args.no_cpu else None
@@ -556,6 +557,8 @@ def run_fireq(args, rank, world, dev):
         line["prefill"] = pre_info
     if c4_info:
         line["c4_llama2_70b_ffn"] = c4_info
+    if attn_info:
+        line["kv4q8_attention"] = attn_info
     if cpu:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
@@ -660,6 +663,39 @@ def prefill_figures(F, dev, stream, peaks):
             "peak_source": "2 x MEASURED_PEAKS bf16_tflops (burst)"}
 
 
+def attention_figures(F, dev, stream, peaks, B=16, N=1024, Hq=32, Hkv=8):
+    """KV4Q8 prefill attention (NEXT f4) on Llama3-8B's attention shape (32 query heads, 8 kv
+    heads, d = 128), B sequences of N tokens, causal: fireq_kv4q8_attention timed over a graph of
+    launches; algorithmic flops = 4 d sum_q (q + 1) per (sequence, head) (S and O, causal)."""
+    fp8_peak = 2.0 * peaks["bf16_tflops"]
+    qb, kb, vb = synth.attention(B, N, Hq, Hkv, synth.layer_seed(6, 0))
+    Q, K, V = (synth.bits_to_torch(x).to(dev) for x in (qb, kb, vb))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    cache = F.KVCache(K, V)
+    torch.cuda.synchronize()
+    cache_ms = (time.perf_counter() - t0) * 1e3
+    xq, beta = F.quantize_act(Q.reshape(B * Hq * N, 128))
+    q_fp8, q_scale = xq.reshape(B, Hq, N, 128), beta.reshape(B, Hq, N)
+    out = torch.empty((B * N, Hq * 128), dtype=torch.bfloat16, device=dev)
+    with torch.cuda.stream(stream):
+        F.kv4q8_attention(q_fp8, q_scale, cache, Hq, out=out, stream=stream)
+    torch.cuda.synchronize()
+    per = 10
+    g = capture(lambda: [F.kv4q8_attention(q_fp8, q_scale, cache, Hq, out=out, stream=stream) for _ in range(per)],
+                stream)
+    ms = time_graphs([g], 10, 2, stream) / (10 * per)
+    flops = 4.0 * 128 * B * Hq * N * (N + 1) / 2
+    tf = flops / (ms * 1e-3) / 1e12
+    del cache, g
+    torch.cuda.empty_cache()
+    return {"workload": f"llama3-8b-attention-prefill-{B}x{N}", "heads": f"{Hq} q / {Hkv} kv, d=128, causal",
+            "kernel": "fireq_kv4q8_attention (INT4 K/V cache, FP8 Q and softmax, Alg. 1 online softmax)",
+            "us": round(ms * 1e3, 2), "tflops_algorithmic": round(tf, 1), "fp8_peak_tflops": fp8_peak,
+            "frac_fp8": round(tf / fp8_peak, 4), "kv_cache_quantize_ms_host_loop": round(cache_ms, 2),
+            "peak_source": "2 x MEASURED_PEAKS bf16_tflops (burst)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -669,6 +705,7 @@ def main():
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the Llama2-70B column-parallel figures")
+    ap.add_argument("--no-attention", action="store_true", help="skip the KV4Q8 attention figures")
     ap.add_argument("--colpar", action="store_true", help="column-parallel path even at N=1 (testing)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -328,7 +328,11 @@ struct StageIter {
 constexpr int kConvUnrollJ = FIREQ_CONV_ROLL >= 1 ? 1 : 4;
 constexpr int kConvUnrollQ = FIREQ_CONV_ROLL >= 2 ? 1 : 4;
 
-template <int NTOK, bool SIGN_SPLIT, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS, int NMMA, int NPH>
+// RES: the residual-add epilogue (fireq_w4a8_gemm_residual) is a separate instantiation --
+// its per-element load in the shared epilogue cost 15% at prefill and 3% at decode when
+// compiled into every kernel (measured).
+template <int NTOK, bool SIGN_SPLIT, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS, int NMMA, int NPH,
+          bool RES = false>
 __global__ void __maxnreg__((NTOK <= 32 ? (NPH == 2 ? 96 : 88) : NTOK <= 64 ? 96 : 128))
 k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__ GemmArgs a0,
             const __grid_constant__ CUtensorMap tmap_x1, const __grid_constant__ GemmArgs a1) {
@@ -834,8 +838,11 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
         int ntile = 0, m0 = 0, n = 0;
         float gam = 1.0f;
         // residual of this thread's channel for the segment's first 16 tokens (bf16 pairs), loaded
-        // at the segment start so its L2 round trip overlaps the mainloop
-        uint32_t rpre[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        // at the segment start so its L2 round trip overlaps the mainloop (decode tiles: the
+        // residual projections at decode; larger tiles load it in the epilogue, where 8 more live
+        // registers would spill the prefill kernels)
+        constexpr bool kResPre = RES && NTOK == 16 && NPH == 1;
+        uint32_t rpre[kResPre ? 8 : 1] = {0};
         const bool use_gam = a.gamma != nullptr || (a.out_layout == 2 && a.gamma_up != nullptr);
         // Step 3 for 16 tokens [m0 + 16 ch, +16) of this thread's output channel n:
         // y = bf16(acc * (beta_m 2^-n) [* gamma_n]).  Y^T rows are 32 contiguous bytes per
@@ -848,9 +855,11 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             for (int c = 0; c < 16; ++c) {
                 float y = __fmul_rn(acc[c], sScale[ch * 16 + c]);
                 if (use_gam) y = __fmul_rn(y, gam);
-                if (a.residual && mb + c < a.M) {
-                    const float rv = ch == 0 ? __uint_as_float(((c & 1) ? (rpre[c >> 1] & 0xFFFF0000u) : (rpre[c >> 1] << 16)))
-                                             : __bfloat162float(a.residual[(size_t)(mb + c) * a.ldr + n]);
+                if (RES && mb + c < a.M) {
+                    const float rv = (kResPre && ch == 0)
+                                         ? __uint_as_float(((c & 1) ? (rpre[(c >> 1) % (kResPre ? 8 : 1)] & 0xFFFF0000u)
+                                                              : (rpre[(c >> 1) % (kResPre ? 8 : 1)] << 16)))
+                                         : __bfloat162float(a.residual[(size_t)(mb + c) * a.ldr + n]);
                     y = __fadd_rn(y, rv);
                 }
                 yb[c] = __float2bfloat16_rn(y);
@@ -925,16 +934,6 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                 gam = (r < 64 || !a.gamma_up) ? 1.0f : __bfloat162float(a.gamma_up[ntile * 64 + (r - 64)]);
             else
                 gam = a.gamma ? a.gamma[n] : 1.0f;
-            if (a.residual) {
-#pragma unroll
-                for (int c = 0; c < 16; ++c) {
-                    uint32_t v = 0u;
-                    // (asm volatile: issued here, not sunk to the use after the accumulator wait)
-                    if (m0 + c < a.M)
-                        asm volatile("ld.global.nc.u16 %0, [%1];" : "=r"(v) : "l"(a.residual + (size_t)(m0 + c) * a.ldr + n));
-                    rpre[c >> 1] = (c & 1) ? (rpre[c >> 1] | (v << 16)) : v;
-                }
-            }
             sScale = sScaleBuf + (sg & 1) * 256;
             for (int t = r; t < NTOK; t += 128)
                 sScale[t] = (m0 + t < a.M) ? __fmul_rn(__bfloat162float(a.x_scale[m0 + t]), p2) : 0.0f;
@@ -954,6 +953,17 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             const int c_lo = whole ? 0 : owner_of(t0, a.U, (int)a.Cs), c_hi = whole ? 0 : owner_of(t1, a.U, (int)a.Cs);
             const bool owner = !whole && (int)blockIdx.x == c_lo;
             const bool keep_own = owner && C::kFixSlots > 0;      // own partial stays in registers
+            // only the CTA that emits this tile (cluster rank 0 / the stream-K owner / a whole tile)
+            if (kResPre && a.residual && (csplit ? cq == 0 : (whole || owner))) {
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    uint32_t v = 0u;
+                    // (asm volatile: issued here, not sunk to the use after the accumulator wait)
+                    if (m0 + c < a.M)
+                        asm volatile("ld.global.nc.u16 %0, [%1];" : "=r"(v) : "l"(a.residual + (size_t)(m0 + c) * a.ldr + n));
+                    rpre[(c >> 1) % (kResPre ? 8 : 1)] = (c & 1) ? (rpre[(c >> 1) % (kResPre ? 8 : 1)] | (v << 16)) : v;
+                }
+            }
             float own[C::kFixSlots > 0 ? NTOK : 1];
             // NTOK > 32: an owner whose split segment is the CTA's last one keeps its partial in
             // TMEM (no later MMA touches the buffer) and stages the contributors' partials through
@@ -1615,11 +1625,12 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, bool allow_cluster = true) {
     return p;
 }
 
-template <int NTOK, bool SS, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS, int NMMA, int NPH = 1>
+template <int NTOK, bool SS, int NCONV, int STAGES, int ASTAGES, int ACCBUF, int GPS, int NMMA, int NPH = 1,
+          bool RES = false>
 fireq_status_t launch_cfg(const CUtensorMap& map, const GemmArgs& args, cudaStream_t stream,
                           const CUtensorMap* map1 = nullptr, const GemmArgs* args1 = nullptr) {
     using C = Cfg<NTOK, SS, NCONV, STAGES, ASTAGES, ACCBUF, GPS, NMMA>;
-    auto kern = k_w4a8_gemm<NTOK, SS, NCONV, STAGES, ASTAGES, ACCBUF, GPS, NMMA, NPH>;
+    auto kern = k_w4a8_gemm<NTOK, SS, NCONV, STAGES, ASTAGES, ACCBUF, GPS, NMMA, NPH, RES>;
     // the attribute is per device (a process may drive several GPUs)
     static bool attr_done[kMaxDevices] = {};
     static int resident[kMaxDevices] = {};     // CTAs of this kernel resident at once on the device
@@ -1749,6 +1760,17 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
         for (int q = 0; q < npeer; ++q) args.Yp[q] = peers[q];
         args.npeer = npeer;
     }
+    if (residual) {
+        if (out_layout != 0) return fail(FIREQ_ERROR_INVALID_VALUE, "residual epilogue: row-major Y only");
+        switch (p.ntok) {
+            case 16:  return launch_cfg<16, true, 3, 8, 3, 2, 2, 1, 1, true>(map, args, stream);
+            case 32:  return launch_cfg<32, true, 3, 7, 3, 2, 2, 1, 1, true>(map, args, stream);
+            case 64:  return launch_cfg<64, true, 2, 5, 2, 2, 2, 1, 1, true>(map, args, stream);
+            case 128: return launch_cfg<128, false, 2, 4, 4, 2, 2, 1, 1, true>(map, args, stream);
+            case 224: return launch_cfg<224, false, 2, 5, 2, 2, 1, 1, 1, true>(map, args, stream);
+            default:  return launch_cfg<192, false, 2, 6, 4, 2, 1, 1, 1, true>(map, args, stream);
+        }
+    }
     switch (p.ntok) {
         // <NTOK, sign-split, converter WGs, SMEM stages, TMEM A stages, accumulators, groups/stage,
         //  MMA-issuing warps, resident activations>
@@ -1852,6 +1874,7 @@ fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_b
 #endif
     if (!split && p1.C == p2.C) {
         // one launch: x quantized in-kernel (phase A), gate_up + SwiGLU, h quantized per CTA, down
+        if (residual) return fail(FIREQ_ERROR_UNSUPPORTED_SHAPE, "FIREQ_FFN_PERSISTENT: no residual epilogue");
         a1.x_in = x;
         a1.ldx_in = ldx;
         a1.x_chan = c_gu;
@@ -1867,10 +1890,12 @@ fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_b
         if (st != FIREQ_SUCCESS) return st;
         st = quantize_act_impl(h, nullptr, M, d_ff, d_ff, nullptr, 0, false, hq, hbeta, stream);
         if (st != FIREQ_SUCCESS) return st;
-        return launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map2, a2, stream);
+    } else {
+        st = launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map1, a1, stream);
+        if (st != FIREQ_SUCCESS) return st;
     }
-    st = launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map1, a1, stream);
-    if (st != FIREQ_SUCCESS) return st;
+    // down: the cluster split-K plan of the standalone GEMM, residual in the epilogue if given
+    if (residual) return launch_cfg<16, true, 3, 8, 3, 2, 2, 1, 1, true>(map2, a2, stream);
     return launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map2, a2, stream);
 }
 

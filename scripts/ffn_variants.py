@@ -12,9 +12,19 @@ tag = f"mode={os.environ.get('FIREQ_FFN_MODE', '4')} persistent={os.environ.get(
 for name, cls in [("chain4", bench.FFN), ("fused", bench.FusedFFN)]:
     ffn = cls(F, 16, 4, dev)
     s = torch.cuda.Stream()
-    for res in (False, True):
+    for res in ((0, 1, 2) if cls is bench.FFN else (0, 1)):
         if cls is bench.FFN:
             def step(r, res=res):
+                if res == 2:                 # the down GEMM with the residual in its epilogue
+                    F.quantize_act(ffn.x, chan_mul=ffn.c_gu, out=(ffn.xq, ffn.beta), stream=s)
+                    p_gu, s_gu, p_d, s_d = ffn.rot[r]
+                    F.w4a8_gemm(ffn.xq, ffn.beta, p_gu, s_gu, 2 * bench.D_FF, ffn.n_gu, gamma=ffn.gamma, out=ffn.gu,
+                                workspace=ffn.ws1, stream=s)
+                    F.silu_mul_quantize_act(ffn.gu[:, :bench.D_FF], ffn.gu[:, bench.D_FF:], out=(ffn.hq, ffn.hbeta),
+                                            stream=s)
+                    F.w4a8_gemm(ffn.hq, ffn.hbeta, p_d, s_d, bench.D_MODEL, ffn.n_d, out=ffn.y, workspace=ffn.ws2,
+                                stream=s, residual=ffn.x)
+                    return
                 ffn.step(r, s)
                 if res:
                     ffn.y.add_(ffn.x)

@@ -144,6 +144,7 @@ def _p2p_rank(rank, world, port, M, N, K, out_dir):
         for it in range(3):                       # repeated calls: the epochs advance
             with torch.cuda.stream(s):
                 symm.yt.zero_()
+                torch.cuda.synchronize()          # zeroed before the peer's stores can arrive
                 dist.barrier()
                 yt = F.w4a8_gemm_colpar_p2p(xq, beta, pl, sl, plan.N_local, qw.n, symm, ws, stream=s)
             torch.cuda.synchronize()
