@@ -855,7 +855,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
             for (int c = 0; c < 16; ++c) {
                 float y = __fmul_rn(acc[c], sScale[ch * 16 + c]);
                 if (use_gam) y = __fmul_rn(y, gam);
-                if (RES && mb + c < a.M) {
+                if (RES && a.residual && mb + c < a.M) {
                     const float rv = (kResPre && ch == 0)
                                          ? __uint_as_float(((c & 1) ? (rpre[(c >> 1) % (kResPre ? 8 : 1)] & 0xFFFF0000u)
                                                               : (rpre[(c >> 1) % (kResPre ? 8 : 1)] << 16)))
@@ -1886,7 +1886,11 @@ fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_b
     if (!tail_quant) {
         a1.amax_out = nullptr;               // the act-quant kernel reduces each row itself
         a1.hq_out = nullptr;
-        st = launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map1, a1, stream);
+        // with a residual the down GEMM runs the RES instantiation; gate_up runs it too (residual
+        // NULL) so that the down kernel's code is still in the instruction caches (a different
+        // kernel function in the chain started ~2.5 us later, measured)
+        st = residual ? launch_cfg<16, true, 3, 8, 3, 2, 2, 1, 1, true>(map1, a1, stream)
+                      : launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map1, a1, stream);
         if (st != FIREQ_SUCCESS) return st;
         st = quantize_act_impl(h, nullptr, M, d_ff, d_ff, nullptr, 0, false, hq, hbeta, stream);
         if (st != FIREQ_SUCCESS) return st;
