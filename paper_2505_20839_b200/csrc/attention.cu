@@ -276,12 +276,13 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
             float mx = -INFINITY;
             if (!diag) {
 #pragma unroll 1
-                for (int c0 = 0; c0 < 64; c0 += 16) {
-                    uint32_t v[16];
+                for (int c0 = 0; c0 < 64; c0 += 32) {          // two loads in flight per wait
+                    uint32_t v[16], v2[16];
                     ptx::tmem_ld_x16(ts + c0, v);
+                    ptx::tmem_ld_x16(ts + c0 + 16, v2);
                     ptx::tmem_wait_ld();
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) mx = fmaxf(mx, __uint_as_float(v[c]));
+                    for (int c = 0; c < 16; ++c) mx = fmaxf(mx, fmaxf(__uint_as_float(v[c]), __uint_as_float(v2[c])));
                 }
             } else {
 #pragma unroll 1
@@ -309,11 +310,13 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
             const uint32_t tp = tmem + lane_base + kTP + s * 32 + hf * 16;
 #pragma unroll 1
             for (int c0 = 0; c0 < 64; c0 += 32) {
-                uint32_t v[16], w8[8];
+                uint32_t vv[2][16], w8[8];
+                ptx::tmem_ld_x16(ts + c0, vv[0]);
+                ptx::tmem_ld_x16(ts + c0 + 16, vv[1]);
+                ptx::tmem_wait_ld();
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
-                    ptx::tmem_ld_x16(ts + c0 + hh * 16, v);
-                    ptx::tmem_wait_ld();
+                    const uint32_t (&v)[16] = vv[hh];
                     float p[16];
 #pragma unroll
                     for (int c = 0; c < 16; ++c) p[c] = ex2_approx(__fmaf_rn(__uint_as_float(v[c]), sc, -off));
