@@ -129,7 +129,7 @@ __device__ __forceinline__ long long prof_clock() {
 #define FIREQ_TRACE2_VAL(slot, v) do { if (a.trace && (slot) < 16) \
     a.trace[a.C * 16 + 512 + blockIdx.x * 16 + (slot)] = (v); } while (0)
 // third per-CTA timeline (phases of the single-launch FFN): trace[C*32 + 512 + cta*16 + slot]
-#define FIREQ_TRACE3(slot) do { if (a0.trace) a0.trace[a0.C * 32 + 512 + blockIdx.x * 16 + (slot)] = gtimer(); } while (0)
+#define FIREQ_TRACE3(slot) do { if (NPH == 2 && a0.trace) a0.trace[a0.C * 32 + 512 + blockIdx.x * 16 + (slot)] = gtimer(); } while (0)
 #else
 #define FIREQ_TRACE3(slot) do { } while (0)
 #define FIREQ_TRACE(slot) do { } while (0)
