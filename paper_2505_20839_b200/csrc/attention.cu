@@ -29,6 +29,7 @@
 namespace fireq {
 using namespace dev;
 bool make_x_map(CUtensorMap* out, const uint8_t* x, int64_t M, int64_t K, int ntok);
+extern unsigned long long* g_trace;
 namespace {
 
 constexpr int kD = 128;                 // head dimension (one 128-group per K row)
@@ -48,7 +49,14 @@ struct AttnArgs {
     int N, Hq, Hkv, B, T;               // T = N / 128
     int causal;
     float tau_log2e;                    // softmax scale tau * log2(e)
+    unsigned long long* trace;          // profile builds: per-tile event clocks of CTA 0
 };
+#ifndef FIREQ_PROFILE
+#define FIREQ_PROFILE 0
+#endif
+// profile builds: trace[tile * 8 + ev] = clock64() in CTA 0 (the heaviest query tile)
+#define ATT_EVT(j, ev) do { if (FIREQ_PROFILE && a.trace && blockIdx.x == 0 && (j) < 64) \
+    a.trace[(j) * 8 + (ev)] = clock64(); } while (0)
 
 // shared memory carve-up (offsets from a 1024-aligned base)
 constexpr int kOffQ = 0;                                 // Q tile, 16 KB, SW128
@@ -225,6 +233,7 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
                 ptx::mma_commit(&pempty[s]);
                 ptx::mma_commit(&vc_empty[sv]);
             }
+            if (lane == 0) ATT_EVT(j, 7);
             __syncwarp();
         };
         for (int j = 0; j < nkv; ++j) {
@@ -241,6 +250,7 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
                 ptx::mma_commit(&s_full[s]);
                 ptx::mma_commit(&kc_empty[sk]);
             }
+            if (lane == 0) ATT_EVT(j, 6);
             __syncwarp();
             if (j > 0) issue_o(j - 1);
         }
@@ -267,7 +277,9 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
         for (int j = 0; j < nkv; ++j) {
             const int s = j & 1, ph = (j >> 1) & 1;
             const bool diag = a.causal && j == i;
+            if (hf == 0 && r == 0) ATT_EVT(j, 0);
             ptx::mbar_wait(&s_full[s], ph);
+            if (hf == 0 && r == 0) ATT_EVT(j, 1);
             ptx::tc_fence_after();
             const uint32_t ts = tmem + lane_base + kTS + s * 128 + hf * 64;
             // m_new = max(m_old, rowmax(x_j)) (lines 10-11), max over the raw accumulators (sc > 0)
@@ -298,6 +310,7 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
             xmax[(s * 2 + hf) * 128 + r] = mx;
             ptx::named_bar_sync(3, 256);
             mx = fmaxf(mx, xmax[(s * 2 + (hf ^ 1)) * 128 + r]);
+            if (hf == 0 && r == 0) ATT_EVT(j, 2);
             const float mnew = fmaxf(m2, mx * sc);
             const float resc = ex2_approx(m2 - mnew);        // s_i = exp(m_old - m_new); 0 on tile 0
             m2 = mnew;
@@ -305,7 +318,9 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
             const float off = mnew - kLog2_448;
             // 448 P_j = exp2(x_j - m_new + log2 448), l += rowsum, P_hat_j = E4M3_RN(448 P_j) (line 13).
             // The P slot was last read by the O MMA of tile j - 2, complete once O(j - 1) is.
+            if (hf == 0 && r == 0) ATT_EVT(j, 3);
             if (j >= 1) ptx::mbar_wait(&pempty[(j - 1) & 1], ((j - 1) >> 1) & 1);
+            if (hf == 0 && r == 0) ATT_EVT(j, 4);
             ptx::tc_fence_after();
             const uint32_t tp = tmem + lane_base + kTP + s * 32 + hf * 16;
 #pragma unroll 1
@@ -358,6 +373,7 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
                 ptx::mbar_arrive(&s_empty[s]);
                 ptx::mbar_arrive(&p_full[s]);
             }
+            if (hf == 0 && r == 0) ATT_EVT(j, 5);
         }
         // epilogue: O = acc * 2^-n_v / (448 l) -> BF16, token-major [B N][ldo] at head h's columns
         xl[hf * 128 + r] = l;
@@ -412,6 +428,7 @@ fireq_status_t kv4q8_attention_impl(const uint8_t* q_fp8, const __nv_bfloat16* q
     args.T = (int)(N / kTile);
     args.causal = causal;
     args.tau_log2e = tau * 1.4426950408889634f;
+    args.trace = FIREQ_PROFILE ? g_trace : nullptr;
     static bool attr_done[kMaxDevices] = {};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)

@@ -496,7 +496,7 @@ class KVCache:
         self.v_pts = torch.zeros((H, 2), dtype=torch.int32, device=dev)
         L = lib()
         need = max(L.fireq_quantize_weight_workspace_bytes(N, d), L.fireq_quantize_weight_workspace_bytes(d, N))
-        ws = torch.zeros(need, dtype=torch.uint8, device=dev)
+        ws = _zeros_on(need, dev, stream)
         Kc = K.reshape(H, N, d).contiguous()
         Vt = V.reshape(H, N, d).transpose(1, 2).contiguous()          # [H][d][N]
         for x in range(H):
@@ -508,6 +508,9 @@ class KVCache:
                                        _ptr(self.k_pts[x]), _ptr(ws), ws.numel(), _stream(stream)), "fireq_quantize_kv")
             _check(L.fireq_quantize_kv(_ptr(Vt[x]), d, N, None, _ptr(self.vt_packed[x]), _ptr(self.vt_scales[x]),
                                        _ptr(self.v_pts[x]), _ptr(ws), ws.numel(), _stream(stream)), "fireq_quantize_kv")
+        if stream is not None:          # the temporaries are freed while the kernels may still run
+            for t in (ws, Kc, Vt):
+                t.record_stream(stream)
 
 
 def kv4q8_attention(q_fp8, q_scale, cache, Hq, causal=True, tau=None, out=None, stream=None):
