@@ -651,12 +651,19 @@ def prefill_figures(F, dev, stream, peaks):
     ms_d = t(lambda: F.w4a8_gemm(ffn.hq, ffn.hbeta, p_d, s_d, D_MODEL, ffn.n_d, out=ffn.y, workspace=ffn.ws2,
                                  stream=stream))
     ms_ffn = t(lambda: ffn.step(0, stream), reps=3)
-    tf_gu = 2 * M * 2 * D_FF * D_MODEL / (ms_gu * 1e-3) / 1e12
-    tf_d = 2 * M * D_MODEL * D_FF / (ms_d * 1e-3) / 1e12
-    tf_ffn = ffn.flops_per_step() / (ms_ffn * 1e-3) / 1e12
+    flops = ffn.flops_per_step()
     del ffn
     torch.cuda.empty_cache()
+    fused = FusedFFN(F, M, 1, dev)       # fireq_ffn_w4a8_decode at prefill M (SwiGLU in gate_up's epilogue)
+    ms_fused = t(lambda: fused.step(0, stream), reps=3)
+    del fused
+    torch.cuda.empty_cache()
+    tf_gu = 2 * M * 2 * D_FF * D_MODEL / (ms_gu * 1e-3) / 1e12
+    tf_d = 2 * M * D_MODEL * D_FF / (ms_d * 1e-3) / 1e12
+    tf_ffn = flops / (ms_ffn * 1e-3) / 1e12
+    tf_fused = flops / (ms_fused * 1e-3) / 1e12
     return {"workload": "llama2-7b-ffn-prefill-16x1024", "ffn_ms": round(ms_ffn, 3), "ffn_tflops": round(tf_ffn, 1),
+            "fused_ffn_api_ms": round(ms_fused, 3), "frac_fused_ffn": round(tf_fused / fp8_peak, 4),
             "gate_up_ms": round(ms_gu, 3), "gate_up_tflops": round(tf_gu, 1), "down_ms": round(ms_d, 3),
             "down_tflops": round(tf_d, 1), "fp8_peak_tflops": fp8_peak,
             "frac_gate_up": round(tf_gu / fp8_peak, 4), "frac_ffn": round(tf_ffn / fp8_peak, 4),

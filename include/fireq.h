@@ -351,8 +351,8 @@ size_t fireq_ffn_workspace_bytes(int64_t M, int64_t d_model, int64_t d_ff);
 
 /*
  * fireq_ffn_w4a8_decode -- a Llama FFN block y = W_down (silu(W_gate x) * (W_up x)) [+ r]
- * at decode batch sizes with Step 3's element-wise operations fused into the
- * GEMM epilogues, as four kernels:
+ * with Step 3's element-wise operations fused into the GEMM epilogues, as four
+ * kernels (the name is historical: any M):
  *   1. fireq_quantize_act(x, c_gu)                      (A1..A3, Eq. 2)
  *   2. gate_up GEMM over the interleaved W_gu (steps 1-3) whose epilogue forms
  *      h = bf16(silu(g) * u * c_down) from the bf16-rounded g and u (exactly
@@ -371,8 +371,9 @@ size_t fireq_ffn_workspace_bytes(int64_t M, int64_t d_model, int64_t d_ff);
  *   h        out, bf16 [M][d_ff]: the SwiGLU output (before quantization).
  *   y        out, bf16 [M][ldy], ldy >= d_model.
  *   next_*   optional L2 prefetch of the next layer's weights (may be NULL).
- * Shapes: 1 <= M <= 16, d_model, d_ff multiples of 128; otherwise
- * FIREQ_ERROR_UNSUPPORTED_SHAPE.  Same arithmetic as the unfused chain
+ * Shapes: M >= 1 (decode batches and prefill; each GEMM takes its own plan for M), d_model,
+ * d_ff multiples of 128; otherwise FIREQ_ERROR_UNSUPPORTED_SHAPE (the two variants below:
+ * M <= 16).  Same arithmetic as the unfused chain
  * (quantize_act -> gemm -> silu_mul_quantize_act -> gemm[_residual]) up to the fp32
  * summation order of split gate_up tiles; y equals
  * fireq_w4a8_gemm[_residual](quantize_act(h), W_down) exactly.

@@ -403,7 +403,7 @@ fireq_status_t fireq_ffn_w4a8_decode(const void* x, int64_t ldx, const void* c_g
                       d_ff <= 65536,
                   FIREQ_ERROR_UNSUPPORTED_SHAPE, "fireq_ffn_w4a8_decode: d_model, d_ff must be multiples of 128");
     FIREQ_REQUIRE(ffn_shape_supported(M, d_model, d_ff), FIREQ_ERROR_UNSUPPORTED_SHAPE,
-                  "fireq_ffn_w4a8_decode: decode batches only (1 <= M <= 16)");
+                  "fireq_ffn_w4a8_decode: M >= 1");
     FIREQ_REQUIRE(aligned16(x) && (!c_gu || aligned16(c_gu)) && (!c_down || aligned16(c_down)) && aligned16(gu_packed) &&
                       aligned16(gu_scales) && aligned16(d_packed) && aligned16(d_scales) && aligned16(h) &&
                       aligned16(y) && ldx % 8 == 0 && ldx >= d_model && ldy % 8 == 0 && ldy >= d_model &&

@@ -1736,32 +1736,10 @@ size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 
 }  // namespace
 
-fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int64_t M, int64_t K,
-                         const uint8_t* w_packed, const uint8_t* w_scales, int64_t N, int32_t pts_n,
-                         const float* gamma, __nv_bfloat16* Y, int64_t ldy, int out_layout, void* ws,
-                         size_t ws_bytes, cudaStream_t stream, const void* pf0, size_t pf0_bytes,
-                         const void* pf1, size_t pf1_bytes, __nv_bfloat16* const* peers, int npeer,
-                         const __nv_bfloat16* residual, int64_t ldr) {
-    const Plan p = make_plan(M, N, K);
-    if (ws_bytes < gemm_workspace_bytes(M, N, K)) return fail(FIREQ_ERROR_WORKSPACE, "GEMM workspace too small");
-    CUtensorMap map;
-    if (!make_x_map(&map, x_fp8, M, K, p.ntok)) return fail(FIREQ_ERROR_CUDA, "cuTensorMapEncodeTiled failed");
-    GemmArgs args = base_args(p, M, N, K, w_packed, w_scales, pts_n, ws, pf0, pf0_bytes, pf1, pf1_bytes);
-    args.x_scale = x_scale;
-    args.gamma = gamma;
-    args.Y = Y;
-    args.ldy = ldy;
-    args.out_layout = out_layout;
-    args.residual = residual;
-    args.ldr = ldr;
-    args.npeer = 0;
-    if (peers && npeer > 1) {
-        if (npeer > 8 || out_layout != 1) return fail(FIREQ_ERROR_INVALID_VALUE, "peer stores: Y^T and <= 8 ranks");
-        for (int q = 0; q < npeer; ++q) args.Yp[q] = peers[q];
-        args.npeer = npeer;
-    }
-    if (residual) {
-        if (out_layout != 0) return fail(FIREQ_ERROR_INVALID_VALUE, "residual epilogue: row-major Y only");
+namespace {
+// The kernel configuration of plan p (RES: the residual-epilogue instantiation).
+fireq_status_t launch_plan(const Plan& p, const CUtensorMap& map, const GemmArgs& args, cudaStream_t stream, bool res) {
+    if (res) {
         switch (p.ntok) {
             case 16:  return launch_cfg<16, true, 3, 8, 3, 2, 2, 1, 1, true>(map, args, stream);
             case 32:  return launch_cfg<32, true, 3, 7, 3, 2, 2, 1, 1, true>(map, args, stream);
@@ -1793,18 +1771,56 @@ fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int
         default:  return launch_cfg<192, false, 2, 6, 4, 2, 1, 1>(map, args, stream);
     }
 }
+}  // namespace
+
+fireq_status_t gemm_impl(const uint8_t* x_fp8, const __nv_bfloat16* x_scale, int64_t M, int64_t K,
+                         const uint8_t* w_packed, const uint8_t* w_scales, int64_t N, int32_t pts_n,
+                         const float* gamma, __nv_bfloat16* Y, int64_t ldy, int out_layout, void* ws,
+                         size_t ws_bytes, cudaStream_t stream, const void* pf0, size_t pf0_bytes,
+                         const void* pf1, size_t pf1_bytes, __nv_bfloat16* const* peers, int npeer,
+                         const __nv_bfloat16* residual, int64_t ldr) {
+    const Plan p = make_plan(M, N, K);
+    if (ws_bytes < gemm_workspace_bytes(M, N, K)) return fail(FIREQ_ERROR_WORKSPACE, "GEMM workspace too small");
+    CUtensorMap map;
+    if (!make_x_map(&map, x_fp8, M, K, p.ntok)) return fail(FIREQ_ERROR_CUDA, "cuTensorMapEncodeTiled failed");
+    GemmArgs args = base_args(p, M, N, K, w_packed, w_scales, pts_n, ws, pf0, pf0_bytes, pf1, pf1_bytes);
+    args.x_scale = x_scale;
+    args.gamma = gamma;
+    args.Y = Y;
+    args.ldy = ldy;
+    args.out_layout = out_layout;
+    args.residual = residual;
+    args.ldr = ldr;
+    args.npeer = 0;
+    if (peers && npeer > 1) {
+        if (npeer > 8 || out_layout != 1) return fail(FIREQ_ERROR_INVALID_VALUE, "peer stores: Y^T and <= 8 ranks");
+        for (int q = 0; q < npeer; ++q) args.Yp[q] = peers[q];
+        args.npeer = npeer;
+    }
+    if (residual && out_layout != 0) return fail(FIREQ_ERROR_INVALID_VALUE, "residual epilogue: row-major Y only");
+    return launch_plan(p, map, args, stream, residual != nullptr);
+}
 
 size_t ffn_workspace_bytes(int64_t M, int64_t d_model, int64_t d_ff) {
-    // gate_up ws | down ws | amax[16] + barriers[4] | x_hat | beta_x | h_hat | beta_h
-    // (neither plan uses clusters: the persistent grid has grid-wide barriers)
+    // gate_up ws | down ws | amax[16] + barriers[8] | x_hat | beta_x | h_hat | beta_h
+    // (each GEMM's workspace covers its plan with and without clusters)
+    const size_t gu = std::max(plan_workspace_bytes(make_plan(M, 2 * d_ff, d_model, false)),
+                               plan_workspace_bytes(make_plan(M, 2 * d_ff, d_model, true)));
     const size_t down = std::max(plan_workspace_bytes(make_plan(M, d_model, d_ff, false)),
                                  plan_workspace_bytes(make_plan(M, d_model, d_ff, true)));
-    return align256(plan_workspace_bytes(make_plan(M, 2 * d_ff, d_model, false))) + align256(down) + 256 +
-           align256((size_t)M * d_model) + 256 + align256((size_t)M * d_ff) + 256;
+    return align256(gu) + align256(down) + 256 + align256((size_t)M * d_model) + align256((size_t)M * 2) +
+           align256((size_t)M * d_ff) + align256((size_t)M * 2);
 }
 
 bool ffn_shape_supported(int64_t M, int64_t d_model, int64_t d_ff) {
-    if (M < 1 || M > 16) return false;
+    (void)d_model; (void)d_ff;
+    return M >= 1;
+}
+
+// the decode-only variants (FIREQ_FFN_MODE=3, FIREQ_FFN_PERSISTENT=1): 16-token tiles, gate_up
+// grid of at most one CTA per SM
+static bool ffn_decode_variant_ok(int64_t M, int64_t d_model, int64_t d_ff) {
+    if (M > 16) return false;
     const Plan p1 = make_plan(M, 2 * d_ff, d_model, /*allow_cluster=*/false);
     return p1.ntok == 16 && p1.C <= sm_count();
 }
@@ -1820,8 +1836,7 @@ fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_b
                                int64_t ldr, __nv_bfloat16* h, __nv_bfloat16* y,
                                int64_t ldy, void* ws, size_t ws_bytes, cudaStream_t stream, const void* pf0,
                                size_t pf0_bytes, const void* pf1, size_t pf1_bytes) {
-    if (!ffn_shape_supported(M, d_model, d_ff))
-        return fail(FIREQ_ERROR_UNSUPPORTED_SHAPE, "fused FFN: decode batches (M <= 16) only");
+    if (!ffn_shape_supported(M, d_model, d_ff)) return fail(FIREQ_ERROR_UNSUPPORTED_SHAPE, "fused FFN: M >= 1");
     if (ws_bytes < ffn_workspace_bytes(M, d_model, d_ff)) return fail(FIREQ_ERROR_WORKSPACE, "FFN workspace too small");
     // Default: four kernels -- act quant(x); gate_up whose epilogue forms h = bf16(silu(g) u);
     // act quant(h) (one CTA per token row: its amax reduction stays inside the CTA); down with
@@ -1834,16 +1849,23 @@ fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_b
     // is ~6 serialized global round trips of ~0.7 us under load (fused decode FFN).
     static const bool split = getenv("FIREQ_FFN_PERSISTENT") == nullptr;
     static const bool tail_quant = getenv("FIREQ_FFN_MODE") && atoi(getenv("FIREQ_FFN_MODE")) == 3;
-    const Plan p1 = make_plan(M, 2 * d_ff, d_model, false), p2 = make_plan(M, d_model, d_ff, split);
+    const bool variant = !split || tail_quant;          // the decode-only variants
+    if (variant && !ffn_decode_variant_ok(M, d_model, d_ff))
+        return fail(FIREQ_ERROR_UNSUPPORTED_SHAPE, "FIREQ_FFN_MODE=3 / FIREQ_FFN_PERSISTENT: M <= 16 only");
+    // (the variants' grid barriers need gate_up without clusters, and the persistent grid a
+    // stream-K down plan of the same grid size)
+    const Plan p1 = make_plan(M, 2 * d_ff, d_model, !variant), p2 = make_plan(M, d_model, d_ff, split);
     uint8_t* w = static_cast<uint8_t*>(ws);
     uint8_t* ws1 = w;
-    uint8_t* ws2 = ws1 + align256(plan_workspace_bytes(p1));
+    const size_t gu_ws = std::max(plan_workspace_bytes(make_plan(M, 2 * d_ff, d_model, false)),
+                                  plan_workspace_bytes(make_plan(M, 2 * d_ff, d_model, true)));
+    uint8_t* ws2 = ws1 + align256(gu_ws);
     const size_t down_ws = std::max(plan_workspace_bytes(make_plan(M, d_model, d_ff, false)),
                                     plan_workspace_bytes(make_plan(M, d_model, d_ff, true)));
     unsigned* amax = reinterpret_cast<unsigned*>(ws2 + align256(down_ws));
     uint8_t* xq = reinterpret_cast<uint8_t*>(amax) + 256;
     __nv_bfloat16* xbeta = reinterpret_cast<__nv_bfloat16*>(xq + align256((size_t)M * d_model));
-    uint8_t* hq = reinterpret_cast<uint8_t*>(xbeta) + 256;
+    uint8_t* hq = reinterpret_cast<uint8_t*>(xbeta) + align256((size_t)M * 2);
     __nv_bfloat16* hbeta = reinterpret_cast<__nv_bfloat16*>(hq + align256((size_t)M * d_ff));
     // phase 0: gate_up over interleaved [gate | up] tiles; SwiGLU epilogue; h quantized in its tail
     CUtensorMap map1, map2;
@@ -1889,8 +1911,7 @@ fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_b
         // with a residual the down GEMM runs the RES instantiation; gate_up runs it too (residual
         // NULL) so that the down kernel's code is still in the instruction caches (a different
         // kernel function in the chain started ~2.5 us later, measured)
-        st = residual ? launch_cfg<16, true, 3, 8, 3, 2, 2, 1, 1, true>(map1, a1, stream)
-                      : launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map1, a1, stream);
+        st = launch_plan(p1, map1, a1, stream, residual != nullptr);
         if (st != FIREQ_SUCCESS) return st;
         st = quantize_act_impl(h, nullptr, M, d_ff, d_ff, nullptr, 0, false, hq, hbeta, stream);
         if (st != FIREQ_SUCCESS) return st;
@@ -1898,9 +1919,8 @@ fireq_status_t ffn_decode_impl(const __nv_bfloat16* x, int64_t ldx, const __nv_b
         st = launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map1, a1, stream);
         if (st != FIREQ_SUCCESS) return st;
     }
-    // down: the cluster split-K plan of the standalone GEMM, residual in the epilogue if given
-    if (residual) return launch_cfg<16, true, 3, 8, 3, 2, 2, 1, 1, true>(map2, a2, stream);
-    return launch_cfg<16, true, 3, 8, 3, 2, 2, 1>(map2, a2, stream);
+    // down: the standalone GEMM's plan (cluster split-K at decode), residual in the epilogue
+    return launch_plan(p2, map2, a2, stream, residual != nullptr);
 }
 
 fireq_status_t debug_lut_table(uint8_t* out, cudaStream_t stream) {

@@ -73,7 +73,7 @@ def test_fused_ffn_host_checks(lib):
     args = lambda M, x: (x, 4096, None, M, 4096, 11008, a16, a16, 0, None, a16, a16, 0, None, 0, a16, a16, 4096,
                          a16, 1 << 20, None, 0, None, 0, None)
     assert lib.fireq_ffn_w4a8_decode(*args(16, None)) == 1               # NULL x
-    assert lib.fireq_ffn_w4a8_decode(*args(17, a16)) == 2                # decode only: M <= 16
+    assert lib.fireq_ffn_w4a8_decode(*args(0, a16)) == 2                 # M >= 1
     assert lib.fireq_ffn_w4a8_decode(*args(16, P(a16.value + 2))) == 3  # misaligned x
     bad_r = list(args(16, a16)); bad_r[13] = a16; bad_r[14] = 100         # residual with ldr < d_model
     assert lib.fireq_ffn_w4a8_decode(*bad_r) == 3
