@@ -350,21 +350,14 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
             }
             // O = s_i * O (line 14) on this half's d columns: O holds tiles 0 .. j-1
             if (j >= 1 && __any_sync(0xffffffffu, resc != 1.0f)) {
-#pragma unroll 1
-                for (int c0 = 0; c0 < 64; c0 += 16) {
-                    const uint32_t to = tmem + lane_base + kTO + hf * 64 + c0;
-                    uint32_t v[16];
-                    ptx::tmem_ld_x16(to, v);
-                    ptx::tmem_wait_ld();
-                    uint32_t lo[8], hi[8];
+                // one 64-column TMEM load and one store (not four dependent round trips)
+                const uint32_t to = tmem + lane_base + kTO + hf * 64;
+                uint32_t o[64];
+                ptx::tmem_ld_x64(to, o);
+                ptx::tmem_wait_ld();
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        lo[c] = __float_as_uint(__uint_as_float(v[c]) * resc);
-                        hi[c] = __float_as_uint(__uint_as_float(v[8 + c]) * resc);
-                    }
-                    ptx::tmem_st_x8(to, lo);
-                    ptx::tmem_st_x8(to + 8, hi);
-                }
+                for (int c = 0; c < 64; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * resc);
+                ptx::tmem_st_x64(to, o);
             }
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
