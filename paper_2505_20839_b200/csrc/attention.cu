@@ -323,32 +323,24 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
             if (hf == 0 && r == 0) ATT_EVT(j, 4);
             ptx::tc_fence_after();
             const uint32_t tp = tmem + lane_base + kTP + s * 32 + hf * 16;
-#pragma unroll 1
-            for (int c0 = 0; c0 < 64; c0 += 32) {
-                uint32_t vv[2][16], w8[8];
-                ptx::tmem_ld_x16(ts + c0, vv[0]);
-                ptx::tmem_ld_x16(ts + c0 + 16, vv[1]);
+            {
+                uint32_t v[64], w16[16];
+                ptx::tmem_ld_x64(ts, v);                      // the half's 64 scores, one load
                 ptx::tmem_wait_ld();
 #pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                    const uint32_t (&v)[16] = vv[hh];
-                    float p[16];
+                for (int c4 = 0; c4 < 16; ++c4) {
+                    float p[4];
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) p[c] = ex2_approx(__fmaf_rn(__uint_as_float(v[c]), sc, -off));
-                    if (diag) {
-#pragma unroll
-                        for (int c = 0; c < 16; ++c)
-                            if (hf * 64 + c0 + hh * 16 + c > r) p[c] = 0.0f;
+                    for (int e = 0; e < 4; ++e) {
+                        const int c = 4 * c4 + e;
+                        p[e] = ex2_approx(__fmaf_rn(__uint_as_float(v[c]), sc, -off));
+                        if (diag && hf * 64 + c > r) p[e] = 0.0f;
+                        l += p[e];
                     }
-#pragma unroll
-                    for (int c = 0; c < 16; ++c) l += p[c];
-#pragma unroll
-                    for (int w = 0; w < 4; ++w)
-                        w8[hh * 4 + w] = e4m3x2_rn(p[4 * w], p[4 * w + 1]) | (e4m3x2_rn(p[4 * w + 2], p[4 * w + 3]) << 16);
+                    w16[c4] = e4m3x2_rn(p[0], p[1]) | (e4m3x2_rn(p[2], p[3]) << 16);
                 }
-                ptx::tmem_st_x8(tp + c0 / 4, w8);
+                ptx::tmem_st_x16(tp, w16);
             }
-            // O = s_i * O (line 14) on this half's d columns: O holds tiles 0 .. j-1
             if (j >= 1 && __any_sync(0xffffffffu, resc != 1.0f)) {
                 // one 64-column TMEM load and one store (not four dependent round trips)
                 const uint32_t to = tmem + lane_base + kTO + hf * 64;
