@@ -287,15 +287,11 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
             // per-element selects out of the others)
             float mx = -INFINITY;
             if (!diag) {
-#pragma unroll 1
-                for (int c0 = 0; c0 < 64; c0 += 32) {          // two loads in flight per wait
-                    uint32_t v[16], v2[16];
-                    ptx::tmem_ld_x16(ts + c0, v);
-                    ptx::tmem_ld_x16(ts + c0 + 16, v2);
-                    ptx::tmem_wait_ld();
+                uint32_t v[64];
+                ptx::tmem_ld_x64(ts, v);                       // one load for the half's 64 scores
+                ptx::tmem_wait_ld();
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) mx = fmaxf(mx, fmaxf(__uint_as_float(v[c]), __uint_as_float(v2[c])));
-                }
+                for (int c = 0; c < 32; ++c) mx = fmaxf(mx, fmaxf(__uint_as_float(v[c]), __uint_as_float(v[32 + c])));
             } else {
 #pragma unroll 1
                 for (int c0 = 0; c0 < 64; c0 += 16) {
