@@ -1559,6 +1559,15 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, bool allow_cluster = true) {
     // its coarser m-tile padding costs > 5% more MMA work than 192-token tiles
     p.ntok = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 192;
     if (M > 128 && 224 * ((M + 223) / 224) * 100 <= 105 * 192 * ((M + 191) / 192)) p.ntok = 224;
+    // mid-M (latency / HBM bound, conversions per MAC do not matter yet): 128-token tiles when
+    // they pad strictly less work than the 192 / 224 choice and N has >= 16 tiles (measured:
+    // M = 256 on 4096 x 14336 24.4 vs 29.4 us, on 14336 x 4096 33.2 vs 42.9; M = 512 on
+    // 4096 x 14336 39.3 vs 41.8, on 4096 x 4096 21.9 vs 24.7; but M = 256 on 1024 x 4096 20.3 vs
+    // 13.0 and M = 400 39 vs 33 (224-token tiles) -- hence the two conditions)
+    static const bool no_mid128 = getenv("FIREQ_NO_MID128") != nullptr;     // A/B switch
+    if (!no_mid128 && M > 128 && M <= 512 && N >= 16 * kTileN &&
+        128 * ((M + 127) / 128) < p.ntok * ((M + p.ntok - 1) / p.ntok))
+        p.ntok = 128;
     p.sign_split = p.ntok <= 64;
     p.m_tiles = (int)((M + p.ntok - 1) / p.ntok);
     p.n_tiles = (int)(N / kTileN);
