@@ -1568,6 +1568,15 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, bool allow_cluster = true) {
     if (!no_mid128 && M > 128 && M <= 512 && N >= 16 * kTileN &&
         128 * ((M + 127) / 128) < p.ntok * ((M + p.ntok - 1) / p.ntok))
         p.ntok = 128;
+#if FIREQ_PROFILE
+    // experiments (profile builds only): force the token-tile size
+    static const int ntok_force = getenv("FIREQ_NTOK_FORCE") ? atoi(getenv("FIREQ_NTOK_FORCE")) : 0;
+#else
+    constexpr int ntok_force = 0;
+#endif
+    if (ntok_force == 16 || ntok_force == 32 || ntok_force == 64 || ntok_force == 128 || ntok_force == 192 ||
+        ntok_force == 224)
+        p.ntok = ntok_force;
     p.sign_split = p.ntok <= 64;
     p.m_tiles = (int)((M + p.ntok - 1) / p.ntok);
     p.n_tiles = (int)(N / kTileN);
