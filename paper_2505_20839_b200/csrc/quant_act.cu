@@ -94,8 +94,11 @@ __device__ __forceinline__ uint4 xprime8(const Src& s, int64_t m, int64_t k) {
 // [rank*K/CL, (rank+1)*K/CL) of token row m; with CL > 1 the row amax is combined across
 // the cluster through distributed shared memory (DSMEM).  The launcher uses CL = 1.  Each
 // thread keeps its (at most R) 8-element vectors of x' in registers between the passes.
-template <int R>
-__global__ void __launch_bounds__(1024) k_act_quant(Src s, int64_t M, int64_t K, int cl,
+// MINB > 1 (large M): at most 512 threads and >= MINB resident CTAs per SM, so the compiler
+// keeps <= 32 registers and enough rows are in flight (with 1024 possible threads it chose 59
+// registers: 2 CTAs per SM, 29% of HBM bandwidth on 16384 x 11008, measured)
+template <int R, int MINB>
+__global__ void __launch_bounds__(MINB > 1 ? 512 : 1024, MINB) k_act_quant(Src s, int64_t M, int64_t K, int cl,
                                                    uint8_t* __restrict__ xq,
                                                    __nv_bfloat16* __restrict__ beta_out,
                                                    unsigned long long* span) {
@@ -163,11 +166,11 @@ __global__ void __launch_bounds__(1024) k_act_quant(Src s, int64_t M, int64_t K,
     span_end(span);
 }
 
-template <int R>
+template <int R, int MINB>
 cudaError_t launch_act(const Src& s, int64_t M, int64_t K, int cl, int threads, uint8_t* xq, __nv_bfloat16* beta,
                        cudaStream_t stream) {
     const unsigned rows = (unsigned)std::min<int64_t>(M, 65535);
-    return launch_ex(k_act_quant<R>, dim3((unsigned)cl, rows), dim3(threads), 0, stream, (unsigned)cl, false, s, M, K, cl,
+    return launch_ex(k_act_quant<R, MINB>, dim3((unsigned)cl, rows), dim3(threads), 0, stream, (unsigned)cl, false, s, M, K, cl,
                      xq, beta, next_span_slot());
 }
 
@@ -255,15 +258,22 @@ fireq_status_t quantize_act_impl(const __nv_bfloat16* X, const __nv_bfloat16* U,
     const int64_t vecs = (K / cl + 7) / 8;
     // decode-sized M: as many threads as vectors (<= 2 per thread); large M: <= 4 per thread
     const int64_t want = M <= 64 ? (vecs + 1) / 2 : (vecs + 3) / 4;
-    const int threads = (int)std::min<int64_t>(1024, std::max<int64_t>(128, (want + 31) / 32 * 32));
+    const bool big = M > 64;
+    const int threads = (int)std::min<int64_t>(big ? 512 : 1024, std::max<int64_t>(128, (want + 31) / 32 * 32));
     const int64_t per = (vecs + threads - 1) / threads;
     cudaError_t e;
-    if (per <= 1) e = launch_act<1>(s, M, K, cl, threads, xq, beta, stream);
-    else if (per <= 2) e = launch_act<2>(s, M, K, cl, threads, xq, beta, stream);
-    else if (per <= 4) e = launch_act<4>(s, M, K, cl, threads, xq, beta, stream);
-    else if (per <= 8) e = launch_act<8>(s, M, K, cl, threads, xq, beta, stream);
-    else if (per <= 16) e = launch_act<16>(s, M, K, cl, threads, xq, beta, stream);
-    else e = launch_act<32>(s, M, K, cl, threads, xq, beta, stream);
+    if (big) {
+        if (per <= 2) e = launch_act<2, 4>(s, M, K, cl, threads, xq, beta, stream);
+        else if (per <= 4) e = launch_act<4, 3>(s, M, K, cl, threads, xq, beta, stream);
+        else if (per <= 8) e = launch_act<8, 2>(s, M, K, cl, threads, xq, beta, stream);
+        else if (per <= 16) e = launch_act<16, 1>(s, M, K, cl, threads, xq, beta, stream);
+        else e = launch_act<32, 1>(s, M, K, cl, threads, xq, beta, stream);
+    } else if (per <= 1) e = launch_act<1, 1>(s, M, K, cl, threads, xq, beta, stream);
+    else if (per <= 2) e = launch_act<2, 1>(s, M, K, cl, threads, xq, beta, stream);
+    else if (per <= 4) e = launch_act<4, 1>(s, M, K, cl, threads, xq, beta, stream);
+    else if (per <= 8) e = launch_act<8, 1>(s, M, K, cl, threads, xq, beta, stream);
+    else if (per <= 16) e = launch_act<16, 1>(s, M, K, cl, threads, xq, beta, stream);
+    else e = launch_act<32, 1>(s, M, K, cl, threads, xq, beta, stream);
     if (e != cudaSuccess) return fail(FIREQ_ERROR_CUDA, std::string("act quant launch: ") + cudaGetErrorString(e));
     return check_launch(mode == 2 ? "fireq_silu_mul_quantize_act" : "fireq_quantize_act");
 }
