@@ -82,3 +82,26 @@ def test_fused_ffn_host_checks(lib):
                                                     a16, 1 << 20, None)
     assert g(None, 4096) == 1 and g(a16, 100) == 3
     assert lib.fireq_interleave_gate_up(a16, a16, 100, 4096, a16, None) == 2
+
+
+def test_kv4q8_host_checks(lib):
+    """fireq_quantize_kv / fireq_kv4q8_attention argument validation (no GPU work)."""
+    P = ctypes.c_void_p
+    buf = ctypes.create_string_buffer(1 << 12)
+    a16 = P((ctypes.addressof(buf) + 15) & ~15)
+    ws = 1 << 20
+    assert lib.fireq_quantize_kv(None, 256, 128, None, a16, a16, a16, a16, ws, None) == 1     # NULL X
+    assert lib.fireq_quantize_kv(a16, 200, 128, None, a16, a16, a16, a16, ws, None) == 2      # N % 128
+    assert lib.fireq_quantize_kv(a16, 256, 128, None, a16, a16, a16, a16, 16, None) == 7      # workspace
+
+    def att(B=1, N=256, Hq=2, Hkv=1, d=128, causal=1, tau=0.088, q=a16, ldo=256):
+        return lib.fireq_kv4q8_attention(q, a16, B, N, Hq, Hkv, d, a16, a16, a16, a16, a16, a16, causal,
+                                         ctypes.c_float(tau), a16, ldo, None)
+    assert att(q=None) == 1                     # NULL q
+    assert att(causal=2) == 1                   # causal must be 0 / 1
+    assert att(tau=0.0) == 1                    # tau > 0
+    assert att(d=64) == 2                       # d = 128 only
+    assert att(N=200) == 2                      # N % 128
+    assert att(Hq=3, Hkv=2) == 2                # Hq % Hkv
+    assert att(ldo=128) == 3                    # ldo >= Hq d
+    assert att(q=P(a16.value + 4)) == 3         # misaligned
