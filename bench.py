@@ -159,17 +159,18 @@ class FFN:
         self.ws1 = F.Workspace(F.gemm_workspace_bytes(M, 2 * D_FF, D_MODEL), dev)
         self.ws2 = F.Workspace(F.gemm_workspace_bytes(M, D_MODEL, D_FF), dev)
 
-    def step(self, r, stream=None, prefetch=os.environ.get("BENCH_PREFETCH", "1") == "1"):
+    def step(self, r, stream=None, prefetch=os.environ.get("BENCH_PREFETCH", "1") == "1", x=None, y=None):
         """One FFN: each GEMM also streams the next GEMM's weights into L2 once its own loads
-        are issued (gate_up -> this step's down; down -> the next step's gate_up)."""
+        are issued (gate_up -> this step's down; down -> the next step's gate_up).
+        x / y: other input / output buffers than self.x / self.y (the pipelined e2e)."""
         F = self.F
         p_gu, s_gu, p_d, s_d = self.rot[r]
         nxt = self.rot[(r + 1) % len(self.rot)]
-        F.quantize_act(self.x, chan_mul=self.c_gu, out=(self.xq, self.beta), stream=stream)
+        F.quantize_act(self.x if x is None else x, chan_mul=self.c_gu, out=(self.xq, self.beta), stream=stream)
         F.w4a8_gemm(self.xq, self.beta, p_gu, s_gu, 2 * D_FF, self.n_gu, gamma=self.gamma, out=self.gu,
                     workspace=self.ws1, stream=stream, prefetch=(p_d, s_d) if prefetch else None)
         F.silu_mul_quantize_act(self.gu[:, :D_FF], self.gu[:, D_FF:], out=(self.hq, self.hbeta), stream=stream)
-        F.w4a8_gemm(self.hq, self.hbeta, p_d, s_d, D_MODEL, self.n_d, out=self.y, workspace=self.ws2, stream=stream,
+        F.w4a8_gemm(self.hq, self.hbeta, p_d, s_d, D_MODEL, self.n_d, out=self.y if y is None else y, workspace=self.ws2, stream=stream,
                     prefetch=(nxt[0], nxt[1]) if prefetch else None)
 
     KERNELS_PER_STEP = 4
@@ -437,23 +438,82 @@ def run_fireq(args, rank, world, dev):
     clocks.stop()
     us_per_step = total_ms * 1e3 / args.steps
 
-    # end to end through host buffers (pinned H2D of x, D2H of y) around the public calls
-    x_host = ffn.x.cpu().pin_memory()
-    y_host = torch.empty_like(ffn.y, device="cpu").pin_memory()
+    # end to end through host buffers: every step copies its own input x_r (pinned host) to the
+    # device, runs the public calls and reads its result y_r back to pinned host memory.
+    # Serial: H2D -> step -> D2H on one stream.  Pipelined (reported as e2e.value): the copies run
+    # on their own streams into double-buffered device x / y, so step r+1's H2D and step r-1's
+    # D2H overlap step r's kernels; the dependencies are H2D_r -> step_r -> D2H_r, and the buffer
+    # reuse edges step_{r-2} -> H2D_r (x) and D2H_{r-2} -> step_r (y).
+    x_hosts = [(ffn.x * (1 + 0.25 * r)).cpu().pin_memory() for r in range(ROTATIONS)]
+    y_hosts = [torch.empty_like(ffn.y, device="cpu").pin_memory() for _ in range(ROTATIONS)]
 
-    def e2e_step(r):
-        ffn.x.copy_(x_host, non_blocking=True)
+    def e2e_serial_step(r):
+        ffn.x.copy_(x_hosts[r], non_blocking=True)
         ffn.step(r, stream)
-        y_host.copy_(ffn.y, non_blocking=True)
+        y_hosts[r].copy_(ffn.y, non_blocking=True)
+
+    s_h2d = torch.cuda.Stream(device=dev)
+    s_d2h = torch.cuda.Stream(device=dev)
+    xd = [torch.empty_like(ffn.x) for _ in range(2)]
+    yd = [torch.empty_like(ffn.y) for _ in range(2)]
+
+    def e2e_pipelined(rs):
+        """Steps rs (a graph body): fork the copy streams from `stream`, join them at the end."""
+        ev = lambda: torch.cuda.Event()  # noqa: E731
+        fork = ev()
+        fork.record(stream)
+        s_h2d.wait_event(fork)
+        s_d2h.wait_event(fork)
+        h2d_done, step_done, d2h_done = {}, {}, {}
+
+        def h2d(i):
+            with torch.cuda.stream(s_h2d):
+                if i - 2 in step_done:
+                    s_h2d.wait_event(step_done[i - 2])
+                xd[i % 2].copy_(x_hosts[rs[i]], non_blocking=True)
+                h2d_done[i] = ev()
+                h2d_done[i].record(s_h2d)
+
+        h2d(0)
+        for i, r in enumerate(rs):
+            if i + 1 < len(rs):
+                h2d(i + 1)
+            stream.wait_event(h2d_done[i])
+            if i - 2 in d2h_done:
+                stream.wait_event(d2h_done[i - 2])
+            ffn.step(r, stream, x=xd[i % 2], y=yd[i % 2])
+            step_done[i] = ev()
+            step_done[i].record(stream)
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(step_done[i])
+                y_hosts[r].copy_(yd[i % 2], non_blocking=True)
+                d2h_done[i] = ev()
+                d2h_done[i].record(s_d2h)
+        stream.wait_stream(s_h2d)
+        stream.wait_stream(s_d2h)
 
     with torch.cuda.stream(stream):
         for r in range(ROTATIONS):
-            e2e_step(r)
+            e2e_serial_step(r)
+        e2e_pipelined(list(range(ROTATIONS)))
     torch.cuda.synchronize()
-    g_e2e_multi = capture(lambda: [e2e_step(r) for r in range(ROTATIONS)], stream)
-    g_e2e = [capture(lambda r=r: e2e_step(r), stream) for r in range(ROTATIONS)]
+    g_e2e_multi = capture(lambda: [e2e_serial_step(r) for r in range(ROTATIONS)], stream)
+    g_e2e = [capture(lambda r=r: e2e_serial_step(r), stream) for r in range(ROTATIONS)]
+    e2e_serial_ms = time_steps(g_e2e_multi, g_e2e, args.steps, args.warmup, stream) / args.steps
+    del g_e2e_multi, g_e2e
+    # 16 steps per graph: the pipeline fills and drains once per graph replay
+    seq = [r % ROTATIONS for r in range(4 * ROTATIONS)]
+    g_e2e_multi = capture(lambda: e2e_pipelined(seq), stream)
+    g_e2e = [capture(lambda r=r: e2e_pipelined([r]), stream) for r in seq]
     e2e_ms = time_steps(g_e2e_multi, g_e2e, args.steps, args.warmup, stream) / args.steps
     del g_e2e_multi, g_e2e
+    # the pipelined result equals the serial one (same inputs, same kernels)
+    y_pipe = [y.clone() for y in y_hosts]
+    with torch.cuda.stream(stream):
+        for r in range(ROTATIONS):
+            e2e_serial_step(r)
+    torch.cuda.synchronize()
+    e2e_same = all(torch.equal(a, b) for a, b in zip(y_pipe, y_hosts))
 
     # ---------------- dominant kernel: the gate_up GEMM alone (HBM bound), rotating weights
     def gu_only(r):
@@ -548,7 +608,9 @@ def run_fireq(args, rank, world, dev):
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"},
         "gemm_down": {"us": round(ms_d * 1e3, 3), "gbs": round(gbs_d, 1), "frac": round(gbs_d / hbm, 4)},
         "e2e": {"value": round(e2e_ms * 1e3, 3), "unit": "us", "h2d_bytes_per_step": ffn.x.numel() * 2,
-                "d2h_bytes_per_step": ffn.y.numel() * 2},
+                "d2h_bytes_per_step": ffn.y.numel() * 2,
+                "mode": "pipelined: per-step H2D / D2H on copy streams, double-buffered device x / y, graphs of 16 steps",
+                "serial_us": round(e2e_serial_ms * 1e3, 3), "pipelined_equals_serial": e2e_same},
         "offline": {"quantize_weight_ms_gate_up_and_down": round(ffn.offline_s * 1e3, 2)},
         "clocks": clocks.summary(),
     }
