@@ -29,11 +29,17 @@ def test_quantize_act_transposed_bit_exact(fireq, M, K):
     assert np.array_equal(q2.cpu().numpy(), rq) and np.array_equal(bits_of(b2), nm.bf16_to_bits(rb))
 
 
-@pytest.mark.parametrize("M,K", [(16, 11008), (5, 256), (200, 1408)])
-def test_silu_mul_quantize(fireq, M, K):
+@pytest.mark.parametrize("M,K,packed", [(16, 11008, False), (5, 256, False), (200, 1408, False),
+                                        (1200, 11008, True), (90, 12288, True)])
+def test_silu_mul_quantize(fireq, M, K, packed):
+    """packed: G and U are the two halves of one [M, 2K] gate_up output (ld = 2K), the prefill
+    layout; M > 64 runs the persistent TMA-ring kernel."""
     gb = synth.activations(M, K, 41)
     ub = synth.activations(M, K, 42)
     G, U = synth.bits_to_torch(gb).to(DEV), synth.bits_to_torch(ub).to(DEV)
+    if packed:
+        GU = torch.cat([G, U], dim=1)
+        G, U = GU[:, :K], GU[:, K:]
     q1, b1 = fireq.silu_mul_quantize_act(G, U)
     q2, b2 = fireq.silu_mul_quantize_act_t(G.t().contiguous(), U.t().contiguous(), M, K)
     assert torch.equal(q1, q2) and torch.equal(b1, b2)          # layouts agree bit-exactly
