@@ -94,6 +94,25 @@ __device__ __forceinline__ uint32_t e4m3x2_rn(float lo, float hi) {
     asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
     return r;
 }
+// SiLU(g) = g / (1 + exp(-g)) as __fdividef(g, 1.0f + __expf(-g)) computes it, written with
+// the flush-to-zero MUFU forms: the non-ftz forms only add denormal range fix-ups, which never
+// change this result (1 + a denormal rounds to 1; 1/(1 + e) is denormal only where
+// __fdividef returns 0 too).  Bitwise equal for every bf16 g against 4096 bf16 u
+// (scripts/silu_ftz_identity.cu, 0 mismatches on the B200).
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float silu_f(float g) {
+    return __fmul_rn(g, rcp_ftz(__fadd_rn(1.0f, ex2_ftz(__fmul_rn(-g, 1.4426950408889634f)))));
+}
+
 // 2^-n for 0 <= n <= 126, exact.
 __device__ __forceinline__ float exp2_neg(int n) { return __int_as_float((127 - n) << 23); }
 

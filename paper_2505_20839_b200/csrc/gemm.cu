@@ -878,6 +878,27 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
 #pragma unroll
                 for (int c = 0; c < 16; ++c) sT[c * kTileN + r] = yb[c];
                 ptx::named_bar_sync(1, 128);
+                if (a.amax_out == nullptr && (a.ldh & 1) == 0) {
+                    // channel pairs: thread (q = r / 32, lane) forms h for channels 2 lane, 2 lane + 1
+                    // of tokens 4q .. 4q + 3 on the packed fp32 path (FMUL2 / FADD2, one F2FP per
+                    // pair) and stores them as one 4-byte word: 128 contiguous bytes per warp store
+                    const int j2 = (r & 31) * 2, q = r >> 5;
+                    const int ch_out = ntile * 64 + j2;
+#pragma unroll
+                    for (int c4 = 0; c4 < 4; ++c4) {
+                        const int c = q * 4 + c4, m = mb + c;
+                        const uint32_t gw = *reinterpret_cast<const uint32_t*>(sT + c * kTileN + j2);
+                        const uint32_t uw = *reinterpret_cast<const uint32_t*>(sT + c * kTileN + 64 + j2);
+                        const float2 gv = make_float2(__uint_as_float(gw << 16), __uint_as_float(gw & 0xFFFF0000u));
+                        const float2 t = __fmul2_rn(gv, make_float2(-1.4426950408889634f, -1.4426950408889634f));
+                        const float2 d = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(ex2_ftz(t.x), ex2_ftz(t.y)));
+                        const float2 sl = __fmul2_rn(gv, make_float2(rcp_ftz(d.x), rcp_ftz(d.y)));   // silu_f, bitwise
+                        const float2 hp = __fmul2_rn(sl, make_float2(__uint_as_float(uw << 16), __uint_as_float(uw & 0xFFFF0000u)));
+                        if (m < a.M)
+                            *reinterpret_cast<__nv_bfloat162*>(a.h_out + (size_t)m * a.ldh + ch_out) =
+                                __floats2bfloat162_rn(hp.x, hp.y);
+                    }
+                } else {
                 const int j = r & 63, half = r >> 6;
                 const int ch_out = ntile * 64 + j;
 #pragma unroll
@@ -885,7 +906,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                     const int c = half * 8 + c8, m = mb + c;
                     const float gv = __bfloat162float(sT[c * kTileN + j]);
                     const float uv = __bfloat162float(sT[c * kTileN + 64 + j]);
-                    const float silu = __fdividef(gv, 1.0f + __expf(-gv));
+                    const float silu = silu_f(gv);     // = __fdividef(gv, 1 + __expf(-gv)), bitwise
                     const __nv_bfloat16 hb = __float2bfloat16_rn(__fmul_rn(silu, uv));
                     float hm = 0.0f;
                     if (m < a.M) {
@@ -896,6 +917,7 @@ k_w4a8_gemm(const __grid_constant__ CUtensorMap tmap_x0, const __grid_constant__
                         for (int o = 16; o; o >>= 1) hm = fmaxf(hm, __shfl_xor_sync(0xffffffffu, hm, o));
                         if (lane == 0 && m < a.M) atomicMax(a.amax_out + m, __float_as_uint(hm));
                     }
+                }
                 }
                 ptx::named_bar_sync(1, 128);
             } else {

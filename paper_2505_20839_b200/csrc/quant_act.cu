@@ -41,25 +41,6 @@ __device__ __forceinline__ float q_div_normal(float x, float beta, float rcp) {
     return __int_as_float(__float_as_int(__fmaf_rn(e, rcp, q0)) | (__float_as_int(x) & 0x80000000));
 }
 
-// SiLU(g) = g / (1 + exp(-g)) as __fdividef(g, 1.0f + __expf(-g)) computes it, written with
-// the flush-to-zero MUFU forms: the non-ftz forms only add denormal range fix-ups, which never
-// change this result (1 + a denormal rounds to 1; 1/(1 + e) is denormal only where
-// __fdividef returns 0 too).  Bitwise equal for every bf16 g against 4096 bf16 u
-// (scripts/silu_ftz_identity.cu, 0 mismatches on the B200).
-__device__ __forceinline__ float ex2_ftz(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-__device__ __forceinline__ float rcp_ftz(float x) {
-    float y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-__device__ __forceinline__ float silu_f(float g) {
-    return __fmul_rn(g, rcp_ftz(__fadd_rn(1.0f, ex2_ftz(__fmul_rn(-g, 1.4426950408889634f)))));
-}
-
 __device__ __forceinline__ float block_max(float v, float* red) {
     for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
