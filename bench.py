@@ -210,12 +210,13 @@ class FusedFFN:
         self.y = torch.empty((M, D_MODEL), dtype=torch.bfloat16, device=dev)
         self.ws = F.Workspace(F.ffn_workspace_bytes(M, D_MODEL, D_FF), dev)
 
-    def step(self, r, stream=None, residual=False):
+    def step(self, r, stream=None, residual=False, x=None, y=None):
         q_gu, q_d = self.rot[r]
         nxt = self.rot[(r + 1) % len(self.rot)][0]
         pf = (nxt.packed, nxt.scales) if os.environ.get("BENCH_PREFETCH", "1") == "1" else None
-        self.F.ffn_w4a8_decode(self.x, q_gu, q_d, h=self.h, out=self.y, workspace=self.ws, stream=stream,
-                               prefetch=pf, residual=self.x if residual else None)
+        x = self.x if x is None else x
+        self.F.ffn_w4a8_decode(x, q_gu, q_d, h=self.h, out=self.y if y is None else y, workspace=self.ws,
+                               stream=stream, prefetch=pf, residual=x if residual else None)
 
     def bytes_per_step(self):
         M = self.M
@@ -418,17 +419,23 @@ def run_fireq(args, rank, world, dev):
         from paper_2505_20839_b200 import multigpu
         return multigpu.run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src, clock_cls=ClockSampler)
 
-    # ---------------- decode FFN (headline): quantize_act, gemm, silu_mul_quantize_act, gemm
+    # ---------------- decode FFN (headline): the FFN block fireq_ffn_w4a8_decode (quantize_act(x);
+    # gate_up with the SwiGLU epilogue; quantize_act(h); down).  The same FFN as the 4-call chain
+    # (quantize_act, gemm, silu_mul_quantize_act, gemm) is timed below as `chain_api_us`.
     ffn = FFN(F, M_DECODE, ROTATIONS, dev)
+    fused = FusedFFN(F, M_DECODE, ROTATIONS, dev)
+    step_bytes = fused.bytes_per_step()
+    h2d_bytes, d2h_bytes = fused.x.numel() * 2, fused.y.numel() * 2
     torch.cuda.synchronize()
     with torch.cuda.stream(stream):
         for r in range(ROTATIONS):          # first launches outside capture (TMA maps, func attrs)
+            fused.step(r, stream)
             ffn.step(r, stream)
     torch.cuda.synchronize()
     # one graph = ROTATIONS consecutive steps (distinct weight copies), PDL edges inside;
     # a remainder uses single-step graphs so that exactly args.steps steps are timed.
-    g_multi = capture(lambda: [ffn.step(r, stream) for r in range(ROTATIONS)], stream)
-    g_single = [capture(lambda r=r: ffn.step(r, stream), stream) for r in range(ROTATIONS)]
+    g_multi = capture(lambda: [fused.step(r, stream) for r in range(ROTATIONS)], stream)
+    g_single = [capture(lambda r=r: fused.step(r, stream), stream) for r in range(ROTATIONS)]
     clocks = ClockSampler(dev.index or 0)
     clocks.start()
     time.sleep(0.25)
@@ -444,18 +451,18 @@ def run_fireq(args, rank, world, dev):
     # on their own streams into double-buffered device x / y, so step r+1's H2D and step r-1's
     # D2H overlap step r's kernels; the dependencies are H2D_r -> step_r -> D2H_r, and the buffer
     # reuse edges step_{r-2} -> H2D_r (x) and D2H_{r-2} -> step_r (y).
-    x_hosts = [(ffn.x * (1 + 0.25 * r)).cpu().pin_memory() for r in range(ROTATIONS)]
-    y_hosts = [torch.empty_like(ffn.y, device="cpu").pin_memory() for _ in range(ROTATIONS)]
+    x_hosts = [(fused.x * (1 + 0.25 * r)).cpu().pin_memory() for r in range(ROTATIONS)]
+    y_hosts = [torch.empty_like(fused.y, device="cpu").pin_memory() for _ in range(ROTATIONS)]
 
     def e2e_serial_step(r):
-        ffn.x.copy_(x_hosts[r], non_blocking=True)
-        ffn.step(r, stream)
-        y_hosts[r].copy_(ffn.y, non_blocking=True)
+        fused.x.copy_(x_hosts[r], non_blocking=True)
+        fused.step(r, stream)
+        y_hosts[r].copy_(fused.y, non_blocking=True)
 
     s_h2d = torch.cuda.Stream(device=dev)
     s_d2h = torch.cuda.Stream(device=dev)
-    xd = [torch.empty_like(ffn.x) for _ in range(2)]
-    yd = [torch.empty_like(ffn.y) for _ in range(2)]
+    xd = [torch.empty_like(fused.x) for _ in range(2)]
+    yd = [torch.empty_like(fused.y) for _ in range(2)]
 
     def e2e_pipelined(rs):
         """Steps rs (a graph body): fork the copy streams from `stream`, join them at the end."""
@@ -481,7 +488,7 @@ def run_fireq(args, rank, world, dev):
             stream.wait_event(h2d_done[i])
             if i - 2 in d2h_done:
                 stream.wait_event(d2h_done[i - 2])
-            ffn.step(r, stream, x=xd[i % 2], y=yd[i % 2])
+            fused.step(r, stream, x=xd[i % 2], y=yd[i % 2])
             step_done[i] = ev()
             step_done[i].record(stream)
             with torch.cuda.stream(s_d2h):
@@ -537,17 +544,11 @@ def run_fireq(args, rank, world, dev):
     gbs_gu = b_gu / (ms_gu * 1e-3) / 1e9
     b_d = gemm_bytes(M_DECODE, D_MODEL, D_FF)
     gbs_d = b_d / (ms_d * 1e-3) / 1e9
-    # ---------------- the same FFN through fireq_ffn_w4a8_decode (3 kernels, SwiGLU fused)
-    fused = FusedFFN(F, M_DECODE, ROTATIONS, dev)
-    torch.cuda.synchronize()
-    with torch.cuda.stream(stream):
-        for r in range(ROTATIONS):
-            fused.step(r, stream)
-    torch.cuda.synchronize()
-    gf_multi = capture(lambda: [fused.step(r, stream) for r in range(ROTATIONS)], stream)
-    gf_single = [capture(lambda r=r: fused.step(r, stream), stream) for r in range(ROTATIONS)]
-    fused_us = time_steps(gf_multi, gf_single, args.steps, args.warmup, stream) * 1e3 / args.steps
-    del gf_multi, gf_single
+    # ---------------- the same FFN as the 4-call chain (quantize_act, gemm, silu_mul_quantize_act, gemm)
+    gc_multi = capture(lambda: [ffn.step(r, stream) for r in range(ROTATIONS)], stream)
+    gc_single = [capture(lambda r=r: ffn.step(r, stream), stream) for r in range(ROTATIONS)]
+    chain_us = time_steps(gc_multi, gc_single, args.steps, args.warmup, stream) * 1e3 / args.steps
+    del gc_multi, gc_single
     # the unfused FFN block: the 4-kernel chain + the residual add as its own kernel
     def chain_res(r):
         ffn.step(r, stream)
@@ -589,14 +590,16 @@ def run_fireq(args, rank, world, dev):
         "scaling": "strong", "vs_baseline": None, "dtype": "fp8e4m3 x int4 -> f32 acc -> bf16", "data": "synthetic",
         "config": {"workload": "llama2-7b-ffn-decode-b16", "tokens": M_DECODE, "d_model": D_MODEL, "d_ff": D_FF,
                    "gemms": "gate_up 22016x4096 (fused, gamma=[1|c_down]) + down 4096x11008",
-                   "api": "fireq_quantize_act, fireq_w4a8_gemm, fireq_silu_mul_quantize_act, fireq_w4a8_gemm",
+                   "api": "fireq_ffn_w4a8_decode (quantize_act(x); gate_up + SwiGLU epilogue; quantize_act(h); "
+                          "down)",
                    "parallelism": "single GPU",
                    "l2": f"{ROTATIONS} rotating weight copies ({ROTATIONS * (b_gu + b_d) / 1e6:.0f} MB > 2x L2)",
                    "graph": f"CUDA graphs of {ROTATIONS} steps (4 PDL-chained kernels per step)"},
-        "gpu_launches": FFN.KERNELS_PER_STEP * args.steps,
-        "step_gbs": round(ffn.bytes_per_step() / (us_per_step * 1e-6) / 1e9, 1),
-        "step_hbm_frac": round(ffn.bytes_per_step() / (us_per_step * 1e-6) / 1e9 / peaks["hbm_gbs"], 4),
-        "fused_ffn_api_us": round(fused_us, 3),
+        "gpu_launches": FusedFFN.KERNELS_PER_STEP * args.steps,
+        "step_gbs": round(step_bytes / (us_per_step * 1e-6) / 1e9, 1),
+        "step_hbm_frac": round(step_bytes / (us_per_step * 1e-6) / 1e9 / peaks["hbm_gbs"], 4),
+        "chain_api_us": round(chain_us, 3),
+        "chain_api": "fireq_quantize_act, fireq_w4a8_gemm, fireq_silu_mul_quantize_act, fireq_w4a8_gemm",
         "ffn_block_residual": {"fused_us": round(fused_res_us, 3), "unfused_chain_plus_add_us": round(chain_res_us, 3),
                                "fused": "fireq_ffn_w4a8_decode: SwiGLU in gate_up's epilogue, residual in down's",
                                "unfused": "the 4-kernel chain + y += x as its own kernel"},
@@ -607,8 +610,8 @@ def run_fireq(args, rank, world, dev):
                      "algorithmic_bytes": b_gu, "launch_us": round(ms_gu * 1e3, 3),
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"},
         "gemm_down": {"us": round(ms_d * 1e3, 3), "gbs": round(gbs_d, 1), "frac": round(gbs_d / hbm, 4)},
-        "e2e": {"value": round(e2e_ms * 1e3, 3), "unit": "us", "h2d_bytes_per_step": ffn.x.numel() * 2,
-                "d2h_bytes_per_step": ffn.y.numel() * 2,
+        "e2e": {"value": round(e2e_ms * 1e3, 3), "unit": "us", "h2d_bytes_per_step": h2d_bytes,
+                "d2h_bytes_per_step": d2h_bytes,
                 "mode": "pipelined: per-step H2D / D2H on copy streams, double-buffered device x / y, graphs of 16 steps",
                 "serial_us": round(e2e_serial_ms * 1e3, 3), "pipelined_equals_serial": e2e_same},
         "offline": {"quantize_weight_ms_gate_up_and_down": round(ffn.offline_s * 1e3, 2)},

@@ -290,8 +290,14 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
                 uint32_t v[64];
                 ptx::tmem_ld_x64(ts, v);                       // one load for the half's 64 scores
                 ptx::tmem_wait_ld();
+                // four independent max chains (a single chain is 32 dependent FMNMX)
+                float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                for (int c = 0; c < 32; ++c) mx = fmaxf(mx, fmaxf(__uint_as_float(v[c]), __uint_as_float(v[32 + c])));
+                for (int c = 0; c < 64; c += 8)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        m4[q] = fmaxf(m4[q], fmaxf(__uint_as_float(v[c + q]), __uint_as_float(v[c + 4 + q])));
+                mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
             } else {
 #pragma unroll 1
                 for (int c0 = 0; c0 < 64; c0 += 16) {
@@ -323,18 +329,27 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
                 uint32_t v[64], w16[16];
                 ptx::tmem_ld_x64(ts, v);                      // the half's 64 scores, one load
                 ptx::tmem_wait_ld();
+                // exponent arguments on the packed FFMA2 path (per element the same RN fma);
+                // the row sum in four independent partial sums (one chain was 64 dependent FADDs)
+                const float2 sc2 = make_float2(sc, sc), noff2 = make_float2(-off, -off);
+                float2 la = make_float2(0.0f, 0.0f), lb = make_float2(0.0f, 0.0f);
 #pragma unroll
                 for (int c4 = 0; c4 < 16; ++c4) {
                     float p[4];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
+                    for (int e = 0; e < 4; e += 2) {
                         const int c = 4 * c4 + e;
-                        p[e] = ex2_approx(__fmaf_rn(__uint_as_float(v[c]), sc, -off));
+                        const float2 t = __ffma2_rn(make_float2(__uint_as_float(v[c]), __uint_as_float(v[c + 1])), sc2, noff2);
+                        p[e] = ex2_approx(t.x);
+                        p[e + 1] = ex2_approx(t.y);
                         if (diag && hf * 64 + c > r) p[e] = 0.0f;
-                        l += p[e];
+                        if (diag && hf * 64 + c + 1 > r) p[e + 1] = 0.0f;
                     }
+                    la = __fadd2_rn(la, make_float2(p[0], p[1]));
+                    lb = __fadd2_rn(lb, make_float2(p[2], p[3]));
                     w16[c4] = e4m3x2_rn(p[0], p[1]) | (e4m3x2_rn(p[2], p[3]) << 16);
                 }
+                l += (la.x + la.y) + (lb.x + lb.y);
                 ptx::tmem_st_x16(tp, w16);
             }
             if (j >= 1 && __any_sync(0xffffffffu, resc != 1.0f)) {
@@ -343,8 +358,13 @@ k_kv4q8_attn(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__
                 uint32_t o[64];
                 ptx::tmem_ld_x64(to, o);
                 ptx::tmem_wait_ld();
+                const float2 rs2 = make_float2(resc, resc);
 #pragma unroll
-                for (int c = 0; c < 64; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * resc);
+                for (int c = 0; c < 64; c += 2) {
+                    const float2 oo = __fmul2_rn(make_float2(__uint_as_float(o[c]), __uint_as_float(o[c + 1])), rs2);
+                    o[c] = __float_as_uint(oo.x);
+                    o[c + 1] = __float_as_uint(oo.y);
+                }
                 ptx::tmem_st_x64(to, o);
             }
             ptx::tmem_wait_st();
