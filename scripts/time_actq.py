@@ -12,7 +12,8 @@ hq = torch.empty((M, 11008), dtype=torch.uint8, device="cuda"); hb = torch.empty
 xq = torch.empty((M, 4096), dtype=torch.uint8, device="cuda"); xb = torch.empty(M, dtype=torch.bfloat16, device="cuda")
 s = torch.cuda.Stream()
 for name, fn in [("silu_mul_quantize_act 16x11008", lambda: F.silu_mul_quantize_act(gu[:, :11008], gu[:, 11008:], out=(hq, hb), stream=s)),
-                 ("quantize_act(c) 16x4096", lambda: F.quantize_act(x, chan_mul=c, out=(xq, xb), stream=s))]:
+                 ("quantize_act(c) 16x4096", lambda: F.quantize_act(x, chan_mul=c, out=(xq, xb), stream=s)),
+                 ("quantize_act 16x11008 (h)", lambda: F.quantize_act(gu[:, :11008], out=(hq, hb), stream=s))]:
     with torch.cuda.stream(s):
         fn()
     torch.cuda.synchronize()
@@ -29,5 +30,5 @@ for name, fn in [("silu_mul_quantize_act 16x11008", lambda: F.silu_mul_quantize_
         e1.record(s)
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / 400
-    nbytes = M * 22016 * 2 + M * 11008 if "silu" in name else M * 4096 * 3
+    nbytes = M * 22016 * 2 + M * 11008 if "silu" in name else (M * 11008 * 3 if "(h)" in name else M * 4096 * 3)
     print(f"{name.replace('16x', str(M) + 'x')}: {us:.2f} us per launch, {nbytes / us / 1e3:.0f} GB/s")
