@@ -206,3 +206,20 @@ def test_fused_ffn_vs_oracle(fireq, with_residual, M):
     yv = y.float().cpu().numpy().astype(np.float64)
     assert og.g4_error(yv, r) <= 2e-2                        # same bound as the unfused chain
     assert og.rel_frobenius(yv, r) < 5e-3
+
+
+@pytest.mark.gpu
+def test_silu_ftz_form_is_bitwise_the_reference_form(tmp_path):
+    """The kernels' SiLU (ex2.approx.ftz / rcp.approx.ftz, paired bf16 rounding) must equal
+    bf16(__fdividef(g, 1 + __expf(-g)) * u) bit for bit: every bf16 g x 4096 bf16 u
+    (scripts/silu_ftz_identity.cu, compiled and run here)."""
+    import os
+    import shutil
+    import subprocess
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    src = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts", "silu_ftz_identity.cu")
+    exe = str(tmp_path / "silu_id")
+    subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-o", exe, src], check=True,
+                   capture_output=True, timeout=300)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0 and " 0 mismatches" in out.stdout, out.stdout + out.stderr
