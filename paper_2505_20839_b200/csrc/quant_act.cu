@@ -215,6 +215,7 @@ cudaError_t launch_act(const Src& s, int64_t M, int64_t K, int cl, int threads, 
 // version of this ring stalled on its two __syncthreads per row (ncu: "barrier" first).
 // Arithmetic: xprime_pair / encode_pair, bitwise the values of xprime8_from / encode8.
 constexpr int kRowMaxStages = 8;
+constexpr uint32_t kRowSmemMax = 200 * 1024 / 2;     // the largest ring: T = 512, two CTAs per SM
 
 // Lean per-pair arithmetic (bf16 pairs unpacked with one integer op each, fp32 pairs on the
 // packed FMUL2 / FFMA2 / FADD2 path); the row max is taken on the fp32 products before their
@@ -393,10 +394,16 @@ template <int MODE, int R, int T>
 cudaError_t launch_rows(const Src& s, int64_t M, int64_t K, int S, uint32_t smem, uint8_t* xq,
                         __nv_bfloat16* beta, cudaStream_t stream) {
     auto kern = k_act_quant_rows<MODE, R, T>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    cudaError_t e;
     int dev = 0, sms = 0, per_sm = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    // the ring never exceeds kRowSmemMax: raise the dynamic shared memory limit once per device
+    static uint32_t smem_set[64] = {};
+    if (dev < 0 || dev >= 64 || smem_set[dev] < smem) {
+        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmemMax)) != cudaSuccess)
+            return e;
+        if (dev >= 0 && dev < 64) smem_set[dev] = kRowSmemMax;
+    }
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T + 32, smem)) != cudaSuccess) return e;
     const int64_t grid = std::min<int64_t>(M, (int64_t)sms * std::max(per_sm, 1));
