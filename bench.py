@@ -461,41 +461,37 @@ def run_fireq(args, rank, world, dev):
 
     s_h2d = torch.cuda.Stream(device=dev)
     s_d2h = torch.cuda.Stream(device=dev)
-    xd = [torch.empty_like(fused.x) for _ in range(2)]
-    yd = [torch.empty_like(fused.y) for _ in range(2)]
+    E2E_GROUP = int(os.environ.get("BENCH_E2E_GROUP", "4"))
+    NBUF = 4 * ROTATIONS                          # one device x / y per step of a 16-step graph
+    xd = [torch.empty_like(fused.x) for _ in range(NBUF)]
+    yd = [torch.empty_like(fused.y) for _ in range(NBUF)]
 
     def e2e_pipelined(rs):
-        """Steps rs (a graph body): fork the copy streams from `stream`, join them at the end."""
+        """Steps rs (a graph body, len(rs) <= NBUF): fork the copy streams from `stream`, join them
+        at the end.  Step i's input is uploaded into its own device buffer on the H2D stream; the
+        compute stream waits for the uploads of a group of E2E_GROUP steps before the group's first
+        step (so the steps inside a group keep their kernel-to-kernel PDL edges), and each step's
+        result is downloaded on the D2H stream as soon as its last kernel is done."""
         ev = lambda: torch.cuda.Event()  # noqa: E731
         fork = ev()
         fork.record(stream)
         s_h2d.wait_event(fork)
         s_d2h.wait_event(fork)
-        h2d_done, step_done, d2h_done = {}, {}, {}
-
-        def h2d(i):
-            with torch.cuda.stream(s_h2d):
-                if i - 2 in step_done:
-                    s_h2d.wait_event(step_done[i - 2])
-                xd[i % 2].copy_(x_hosts[rs[i]], non_blocking=True)
-                h2d_done[i] = ev()
+        h2d_done = []
+        with torch.cuda.stream(s_h2d):
+            for i, r in enumerate(rs):
+                xd[i].copy_(x_hosts[r], non_blocking=True)
+                h2d_done.append(ev())
                 h2d_done[i].record(s_h2d)
-
-        h2d(0)
         for i, r in enumerate(rs):
-            if i + 1 < len(rs):
-                h2d(i + 1)
-            stream.wait_event(h2d_done[i])
-            if i - 2 in d2h_done:
-                stream.wait_event(d2h_done[i - 2])
-            fused.step(r, stream, x=xd[i % 2], y=yd[i % 2])
-            step_done[i] = ev()
-            step_done[i].record(stream)
+            if i % E2E_GROUP == 0:
+                stream.wait_event(h2d_done[min(i + E2E_GROUP, len(rs)) - 1])
+            fused.step(r, stream, x=xd[i], y=yd[i])
+            done = ev()
+            done.record(stream)
             with torch.cuda.stream(s_d2h):
-                s_d2h.wait_event(step_done[i])
-                y_hosts[r].copy_(yd[i % 2], non_blocking=True)
-                d2h_done[i] = ev()
-                d2h_done[i].record(s_d2h)
+                s_d2h.wait_event(done)
+                y_hosts[r].copy_(yd[i], non_blocking=True)
         stream.wait_stream(s_h2d)
         stream.wait_stream(s_d2h)
 
@@ -612,7 +608,7 @@ def run_fireq(args, rank, world, dev):
         "gemm_down": {"us": round(ms_d * 1e3, 3), "gbs": round(gbs_d, 1), "frac": round(gbs_d / hbm, 4)},
         "e2e": {"value": round(e2e_ms * 1e3, 3), "unit": "us", "h2d_bytes_per_step": h2d_bytes,
                 "d2h_bytes_per_step": d2h_bytes,
-                "mode": "pipelined: per-step H2D / D2H on copy streams, double-buffered device x / y, graphs of 16 steps",
+                "mode": f"pipelined: per-step H2D / D2H on copy streams into per-step device buffers, the compute stream waits for the uploads of {E2E_GROUP} steps at a time; graphs of 16 steps",
                 "serial_us": round(e2e_serial_ms * 1e3, 3), "pipelined_equals_serial": e2e_same},
         "offline": {"quantize_weight_ms_gate_up_and_down": round(ffn.offline_s * 1e3, 2)},
         "clocks": clocks.summary(),
