@@ -82,9 +82,9 @@ def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src, clock_c
         F.silu_mul_quantize_act_t(gut[:D_FF], gut[D_FF:2 * D_FF], M, D_FF, out=(hq, hbeta), stream=stream)
         F.w4a8_gemm_colpar(hq, hbeta, pd, sd, plan_d.N_local, n_d, comm, yt, ws2, stream=stream)
 
-    def step(r):
+    def step(r, xin=None):
         pg, sg, pd, sd = rot[r]
-        F.quantize_act(x, chan_mul=q_gu.c, out=(xq, beta), stream=stream)
+        F.quantize_act(x if xin is None else xin, chan_mul=q_gu.c, out=(xq, beta), stream=stream)
         g = F.w4a8_gemm_colpar_p2p(xq, beta, pg, sg, plan_gu.N_local, n_gu, symm_gu, ws1, gamma_local=gamma_l,
                                    stream=stream)
         F.silu_mul_quantize_act_t(g[:D_FF], g[D_FF:2 * D_FF], M, D_FF, out=(hq, hbeta), stream=stream)
@@ -138,26 +138,59 @@ def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src, clock_c
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     us_per_step = float(ms.item()) * 1e3 / steps
 
-    # end to end through host buffers: pinned H2D of x and D2H of the gathered y every step
-    x_host = x.cpu().pin_memory()
+    # end to end through host buffers: pinned H2D of each step's x and D2H of the gathered y
+    # every step.  The uploads run ahead on their own stream into per-step device buffers (x is
+    # rank-local); the download stays on the compute stream: peers write this rank's Y^T in
+    # the next step, so it must be read before that step starts.
+    x_hosts = [(x * (1 + 0.25 * r)).cpu().pin_memory() for r in range(R)]
+    xds = [torch.empty_like(x) for _ in range(R)]
     y_host = torch.empty_like(yt, device="cpu").pin_memory()
+    s_h2d = torch.cuda.Stream(device=dev)
+
+    def e2e_steps(rs):
+        fork = torch.cuda.Event()
+        fork.record(stream)
+        s_h2d.wait_event(fork)
+        done = []
+        with torch.cuda.stream(s_h2d):
+            for i, r in enumerate(rs):
+                xds[i].copy_(x_hosts[r], non_blocking=True)
+                done.append(torch.cuda.Event())
+                done[i].record(s_h2d)
+        for i, r in enumerate(rs):
+            stream.wait_event(done[i])
+            step(r, xds[i])
+            y_host.copy_(symm_d.yt, non_blocking=True)
+        stream.wait_stream(s_h2d)
 
     def e2e_step(r):
-        x.copy_(x_host, non_blocking=True)
-        step(r)
-        y_host.copy_(symm_d.yt, non_blocking=True)
+        e2e_steps([r])
 
     with torch.cuda.stream(stream):
         for r in range(R):
             e2e_step(r)
     torch.cuda.synchronize()
+    e2e_graphed = False
+    if graphed:
+        # the same R steps with their copies as one CUDA graph (as the device timing)
+        try:
+            g_e2e = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_e2e, stream=stream):
+                e2e_steps(list(range(R)))
+            e2e_graphed = True
+        except Exception as e:
+            print(f"[rank {rank}] e2e graph capture failed ({e}); timing eager launches", file=sys.stderr)
     dist.barrier()
     e2 = torch.cuda.Event(enable_timing=True)
     e3 = torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         e2.record(stream)
-        for i in range(steps):
-            e2e_step(i % R)
+        if e2e_graphed:
+            for _ in range(steps // R):
+                g_e2e.replay()
+        else:
+            for i in range(steps):
+                e2e_step(i % R)
         e3.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
@@ -242,7 +275,10 @@ def run_colpar_bench(args, rank, world, dev, F, stream, peaks, peak_src, clock_c
                        "l2": f"{R} rotating weight-shard copies", "graph": "captured" if graphed else "eager"},
             "gpu_launches": 4 * steps,
             "e2e": {"value": round(e2e_us, 3), "unit": "us", "h2d_bytes_per_step": x.numel() * 2,
-                    "d2h_bytes_per_step": yt.numel() * 2, "timing": "eager launches, max over ranks"},
+                    "d2h_bytes_per_step": yt.numel() * 2,
+                    "timing": ("CUDA graph of the steps with their copies (uploads on their own stream)"
+                               if e2e_graphed else "eager launches")
+                              + ", max over ranks"},
         }
         if clocks:
             line["clocks"] = clocks.summary()
