@@ -600,6 +600,9 @@ def run_fireq(args, rank, world, dev):
                                "fused": "fireq_ffn_w4a8_decode: SwiGLU in gate_up's epilogue, residual in down's",
                                "unfused": "the 4-kernel chain + y += x as its own kernel"},
         "roofline": {"bound": "hbm", "kernel": "fireq_w4a8_gemm gate_up M=16 N=22016 K=4096",
+                     "kernel_note": "the step's dominant kernel is this GEMM with the SwiGLU pair epilogue inside "
+                                    "fireq_ffn_w4a8_decode (not callable alone); timed here through fireq_w4a8_gemm "
+                                    "with the plain epilogue, same weights, same mainloop",
                      "achieved": round(gbs_gu, 1), "peak": hbm, "unit": "GB/s", "frac": round(gbs_gu / hbm, 4),
                      "traffic": traffic, "traffic_source": "stored: profiles/traffic.json, ncu --set full "
                      "dram__bytes_read.sum + dram__bytes_write.sum of this kernel (not measured in this run)",
