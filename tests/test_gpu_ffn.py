@@ -208,6 +208,22 @@ def test_fused_ffn_vs_oracle(fireq, with_residual, M):
     assert og.rel_frobenius(yv, r) < 5e-3
 
 
+def test_fused_ffn_headline_size_vs_oracle(fireq):
+    """The bench's headline step at its full size (Llama2-7B FFN, batch 16: d = 4096,
+    d_ff = 11008) through fireq_ffn_w4a8_decode, every output against the oracle's FFN
+    (same bound as the chain)."""
+    M, d, dff = 16, 4096, 11008
+    wg, wu, wd, xb, *_, qil, qd, x = _ffn_case(fireq, M, d, dff, 91)
+    y = fireq.ffn_w4a8_decode(x, qil, qd, workspace=fireq.Workspace(fireq.ffn_workspace_bytes(M, d, dff)))
+    torch.cuda.synchronize()
+    ref_gu = oq.quantize_weight(synth.bits_to_f64(np.concatenate([wg, wu], axis=0)), 1)
+    ref_d = oq.quantize_weight(synth.bits_to_f64(wd), 1)
+    _, r = of.ffn_reference(synth.bits_to_f64(xb), ref_gu, ref_d, dff)
+    yv = y.float().cpu().numpy().astype(np.float64)
+    assert og.g4_error(yv, r) <= 2e-2
+    assert og.rel_frobenius(yv, r) < 5e-3
+
+
 @pytest.mark.gpu
 def test_silu_ftz_form_is_bitwise_the_reference_form(tmp_path):
     """The kernels' SiLU (ex2.approx.ftz / rcp.approx.ftz, paired bf16 rounding) must equal
