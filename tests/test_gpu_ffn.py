@@ -224,6 +224,25 @@ def test_fused_ffn_headline_size_vs_oracle(fireq):
     assert og.rel_frobenius(yv, r) < 5e-3
 
 
+def test_fused_ffn_prefill_size_sampled_vs_oracle(fireq):
+    """The prefill FFN block at the bench's size (16 x 1024 tokens, d = 4096, d_ff = 11008:
+    224-token tiles, the row-ring quantizers) against the oracle on sampled token rows (every
+    step of the FFN is row-independent, so the oracle runs on those rows only)."""
+    M, d, dff = 16384, 4096, 11008
+    wg, wu, wd, xb, *_, qil, qd, x = _ffn_case(fireq, M, d, dff, 93)
+    y = fireq.ffn_w4a8_decode(x, qil, qd, workspace=fireq.Workspace(fireq.ffn_workspace_bytes(M, d, dff)),
+                              residual=x)
+    torch.cuda.synchronize()
+    rows = np.array([0, 1, 223, 224, 5000, 8191, 12345, 16383])
+    ref_gu = oq.quantize_weight(synth.bits_to_f64(np.concatenate([wg, wu], axis=0)), 1)
+    ref_d = oq.quantize_weight(synth.bits_to_f64(wd), 1)
+    xs = synth.bits_to_f64(xb[rows])
+    _, r = of.ffn_reference(xs, ref_gu, ref_d, dff, residual=xs)
+    yv = y[torch.from_numpy(rows).to(DEV)].float().cpu().numpy().astype(np.float64)
+    assert og.g4_error(yv, r) <= 2e-2
+    assert og.rel_frobenius(yv, r) < 5e-3
+
+
 @pytest.mark.gpu
 def test_silu_ftz_form_is_bitwise_the_reference_form(tmp_path):
     """The kernels' SiLU (ex2.approx.ftz / rcp.approx.ftz, paired bf16 rounding) must equal
