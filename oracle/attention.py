@@ -32,7 +32,7 @@ as the linear layers.  Readings (R30-R37):
 """
 import numpy as np
 
-from .numerics import bf16_rn, e4m3_rn, e4m3_encode
+from .numerics import bf16_rn, e4m3_rn, e4m3_encode, E4M3_POS_GRID
 from . import gemm, quant
 
 
@@ -86,11 +86,31 @@ class KV4Head:
         self.vt_deq = gemm.dequantize_weight(self.vt.packed, self.vt.scales, d, N)
 
 
-def attention_head(Q, kv, t=None, causal=True, tau=None, bc=128):
+def e4m3_rounding_ambiguity(v, delta):
+    """v = 448 P >= 0 (the FP8 softmax argument).  E4M3_RN(v) is decided by which side of the
+    midpoint between its two grid neighbours v lies; an exp evaluated to a relative error
+    below delta (the GPU's fp32 argument and ex2.approx, DESIGN R37) may land on the other
+    side when |v - midpoint| <= delta * v.  Returns (other neighbour - E4M3_RN(v)) there, 0
+    elsewhere -- the largest change of that P_hat code either side may make."""
+    v = np.asarray(v, dtype=np.float64)
+    c = e4m3_rn(v)
+    idx = np.searchsorted(E4M3_POS_GRID, c)
+    up = E4M3_POS_GRID[np.minimum(idx + 1, len(E4M3_POS_GRID) - 1)]
+    dn = E4M3_POS_GRID[np.maximum(idx - 1, 0)]
+    other = np.where(v >= c, up, dn)
+    mid = 0.5 * (c + other)
+    amb = (other != c) & (np.abs(v - mid) <= delta * v)
+    return np.where(amb, other - c, 0.0)
+
+
+def attention_head(Q, kv, t=None, causal=True, tau=None, bc=128, amb_delta=None):
     """One query head against one KV4 head, Alg. 1 step by step with B_c = bc:
     running row max m, P_j = exp(x_j - m_new) quantized to FP8 per kv tile, O = s * O + P_hat_j V_j,
     l = s * l + rowsum(P_j), s = exp(m_old - m_new).  Q [N][d] bf16 values (post-RoPE).
-    Returns (O bf16 values [N][d], O fp64 before the BF16 rounding, dict of intermediates)."""
+    Returns (O bf16 values [N][d], O fp64 before the BF16 rounding, dict of intermediates).
+    amb_delta: also return dict["ambiguity"] [N][d], the largest |O| change the P_hat codes
+    within relative amb_delta of an E4M3 midpoint can make (e4m3_rounding_ambiguity, carried
+    through the same recurrence as O with absolute values)."""
     Q = np.asarray(Q, dtype=np.float64)
     N, d = Q.shape
     tau = 1.0 / np.sqrt(d) if tau is None else tau
@@ -104,6 +124,7 @@ def attention_head(Q, kv, t=None, causal=True, tau=None, bc=128):
     l = np.zeros(N)
     O = np.zeros((N, d))
     p_codes = np.zeros((N, N), dtype=np.uint8)
+    A = np.zeros((N, d)) if amb_delta is not None else None
     with np.errstate(invalid="ignore"):
         for j0 in range(0, N, bc):
             xj = x[:, j0:j0 + bc]
@@ -115,9 +136,14 @@ def attention_head(Q, kv, t=None, causal=True, tau=None, bc=128):
             p_codes[:, j0:j0 + bc] = pc
             O = s[:, None] * O + gemm.gemm_reference(pc, np.ones(N), None, None, d, bc, 0,
                                                      w_deq=kv.vt_deq[:, j0:j0 + bc])
+            if A is not None:
+                dP = np.abs(e4m3_rounding_ambiguity(448.0 * Pj, amb_delta))
+                A = s[:, None] * A + dP @ np.abs(kv.vt_deq[:, j0:j0 + bc]).T
             m = m_new
     O = O * 2.0 ** (-kv.vt.n) / 448.0 / l[:, None]
-    return bf16_rn(O), O, dict(q_codes=q_codes, beta_q=beta_q, S=S, m=m, l=l, p_codes=p_codes)
+    if A is not None:
+        A = A * 2.0 ** (-kv.vt.n) / 448.0 / l[:, None]
+    return bf16_rn(O), O, dict(q_codes=q_codes, beta_q=beta_q, S=S, m=m, l=l, p_codes=p_codes, ambiguity=A)
 
 
 def attention_unquantized(Q, K, V, causal=True, tau=None):

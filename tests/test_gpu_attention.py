@@ -15,6 +15,18 @@ from oracle import numerics as nm
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
 D = 128
+# The GPU forms 448 P = ex2(fp32 argument): relative to the oracle's fp64 exp its argument
+# carries |x| 2^-24 of rounding (|x| < 2^8 here) and ex2.approx ~2^-22, so a P_hat code may
+# round the other way where 448 P lies within 2^-15 (relative) of an E4M3 midpoint (R37).
+AMB_DELTA = 2.0 ** -15
+
+
+def g4_allowing_ambiguous_codes(y, r, amb):
+    """G4 after subtracting, per element, the oracle's bound on what the ambiguous P_hat codes
+    can change (oracle.attention.attention_head(..., amb_delta) -> dict["ambiguity"])."""
+    rms = np.sqrt(np.mean(r * r, axis=1, keepdims=True))
+    den = np.maximum(np.abs(r), 0.1 * rms)
+    return float((np.maximum(np.abs(y - r) - amb, 0.0) / den).max())
 
 
 def crs_calibration(K):
@@ -59,12 +71,32 @@ def test_kv4q8_attention_vs_oracle(fireq, B, N, Hq, Hkv, causal):
             assert np.array_equal(cache.vt_scales[x].cpu().numpy(), kv.vt.scales)
             assert cache.k_pts[x, 0].item() == kv.k.n and cache.v_pts[x, 0].item() == kv.vt.n
             for h in range(hk * g, (hk + 1) * g):
-                _, r, st = oa.attention_head(Q[b, h], kv, t=t[hk], causal=causal)
+                _, r, st = oa.attention_head(Q[b, h], kv, t=t[hk], causal=causal, amb_delta=AMB_DELTA)
                 assert np.array_equal(q_fp8[b, h].cpu().numpy(), st["q_codes"])
                 y = Og[b * N:(b + 1) * N, h * D:(h + 1) * D]
-                e = og.g4_error(y, r)
+                e = g4_allowing_ambiguous_codes(y, r, st["ambiguity"])
                 assert e <= 1e-2, (b, h, e)
                 assert og.rel_frobenius(y, r) < 5e-3
+
+
+def test_kv4q8_attention_bench_size_sampled(fireq):
+    """The bench's attention workload (Llama3-8B prefill: 16 sequences x 1024 tokens, 32 query /
+    8 kv heads, causal) in one launch; sampled (sequence, query head) pairs against the oracle."""
+    B, N, Hq, Hkv = 16, 1024, 32, 8
+    Q, K, V, t, cache, q_fp8, q_scale, O = run(fireq, B, N, Hq, Hkv, True, seed=4242)
+    g = Hq // Hkv
+    Og = O.float().cpu().numpy().astype(np.float64)
+    for b, h in [(0, 0), (3, 9), (7, 13), (12, 22), (15, 31)]:
+        hk = h // g
+        kv = oa.KV4Head(K[b, hk], V[b, hk], t=t[hk])
+        x = b * Hkv + hk
+        assert np.array_equal(cache.k_packed[x].cpu().numpy(), kv.k.packed)
+        assert np.array_equal(cache.vt_packed[x].cpu().numpy(), kv.vt.packed)
+        _, r, st = oa.attention_head(Q[b, h], kv, t=t[hk], causal=True, amb_delta=AMB_DELTA)
+        assert np.array_equal(q_fp8[b, h].cpu().numpy(), st["q_codes"])
+        y = Og[b * N:(b + 1) * N, h * D:(h + 1) * D]
+        assert g4_allowing_ambiguous_codes(y, r, st["ambiguity"]) <= 1e-2, (b, h, og.g4_error(y, r))
+        assert og.rel_frobenius(y, r) < 5e-3
 
 
 def test_kv4q8_attention_repeatable_and_head_layout(fireq):

@@ -148,3 +148,49 @@ def test_g4_rejects_attention_bugs(bug):
     kv = oa.KV4Head(K, V)
     _, O, st = oa.attention_head(Q, kv)
     assert og.g4_error(_two_pass(st["S"], kv, 256, bug), O) > 5e-2
+
+
+def test_e4m3_rounding_ambiguity_brute_force():
+    """Nonzero exactly where v lies within delta * v of the midpoint between E4M3_RN(v) and its
+    neighbour on v's side, and then equal to (that neighbour - E4M3_RN(v)): checked against a
+    brute-force scan of the grid."""
+    rng = np.random.default_rng(5)
+    grid = nm.E4M3_POS_GRID
+    mids = 0.5 * (grid[1:] + grid[:-1])
+    delta = 2.0 ** -15
+    # values at, just around and far from every midpoint, plus random values and the ends
+    v = np.concatenate([mids, mids * (1 + 0.5 * delta), mids * (1 - 0.5 * delta), mids * (1 + 4 * delta),
+                        mids * (1 - 4 * delta), rng.uniform(0, 448, 2000), [0.0, 448.0, 2.0 ** -9]])
+    got = oa.e4m3_rounding_ambiguity(v, delta)
+    for x, g in zip(v, got):
+        c = float(nm.e4m3_rn(np.array([x]))[0])
+        near = [m for m in mids if abs(x - m) <= delta * x]
+        if not near:
+            assert g == 0.0, x
+        else:
+            m = near[0]
+            lo, hi = grid[grid < m].max(), grid[grid > m].min()
+            assert {c, c + g} == {lo, hi}, (x, c, g)
+
+
+def test_attention_ambiguity_bound_is_zero_without_slack_and_covers_code_flips():
+    """amb_delta = 0 on random data: no P value sits exactly on a midpoint, so the bound is 0;
+    with a slack, flipping every ambiguous code of a one-tile head (recomputing O by hand from
+    the oracle's own intermediates) moves O by no more than the bound."""
+    rng = np.random.default_rng(8)
+    N, d = 128, 128
+    Q = nm.bf16_rn(rng.normal(0, 1, (N, d)))
+    K = nm.bf16_rn(rng.normal(0, 1, (N, d)))
+    V = nm.bf16_rn(rng.normal(0, 1, (N, d)))
+    kv = oa.KV4Head(K, V)
+    _, _, st0 = oa.attention_head(Q, kv, causal=True, amb_delta=0.0)
+    assert np.all(st0["ambiguity"] == 0.0)
+    delta = 2.0 ** -6                                  # a large slack: many ambiguous codes
+    _, O, st = oa.attention_head(Q, kv, causal=True, amb_delta=delta)
+    x = st["S"] / np.sqrt(d)
+    x = np.where(np.arange(N)[None, :] <= np.arange(N)[:, None], x, -np.inf)
+    P = np.exp(x - st["m"][:, None])                   # one tile: m is the tile's max
+    dP = oa.e4m3_rounding_ambiguity(448.0 * P, delta)
+    assert np.count_nonzero(dP) > 0
+    O_flip = O + (dP @ kv.vt_deq.T) * 2.0 ** (-kv.vt.n) / 448.0 / st["l"][:, None]
+    assert np.all(np.abs(O_flip - O) <= st["ambiguity"] * (1 + 1e-12) + 1e-300)
