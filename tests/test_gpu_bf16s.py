@@ -81,3 +81,24 @@ def test_gemm_bf16s_deterministic(fireq):
     b = fireq.w4a8_gemm_bf16s(xq, beta, qw.packed, qw.scales, N, qw.n)
     assert torch.equal(a, b)
 
+
+
+@pytest.mark.parametrize("M,N,K", [(16, 22016, 4096), (16, 4096, 11008), (4096, 22016, 4096)])
+def test_gemm_bf16s_timed_shapes_sampled(fireq, M, N, K):
+    """The shapes scripts/time_bf16s.py times (the Llama2-7B FFN GEMMs at decode and prefill):
+    the weight quantizer bit-exact, the GEMM within G4 on sampled token rows (rows are
+    independent, so the oracle runs on those rows only)."""
+    seed = M + N + K
+    wb = synth.weights(N, K, synth.layer_seed(14, seed))
+    xb = synth.activations(M, K, synth.layer_seed(15, seed))
+    qw, ref = check_weight_bf16s(fireq, wb, 1)
+    xq, beta = fireq.quantize_act(synth.bits_to_torch(xb).to(DEV), chan_mul=qw.c)
+    Y = fireq.w4a8_gemm_bf16s(xq, beta, qw.packed, qw.scales, N, qw.n)
+    torch.cuda.synchronize()
+    rows = np.unique(np.array([0, 1, M // 2, M - 1, min(M - 1, 127), min(M - 1, 128)]))
+    rq, rbeta = oq.quantize_act(synth.bits_to_f64(xb[rows]), ref.c)
+    assert np.array_equal(xq[torch.from_numpy(rows).to(DEV)].cpu().numpy(), rq)
+    r = og.gemm_reference_bf16s(rq, rbeta, ref.codes, ref.sigma, ref.n)
+    y = Y[torch.from_numpy(rows).to(DEV)].float().cpu().numpy().astype(np.float64)
+    assert og.g4_error(y, r) <= G4_TOL
+    assert og.rel_frobenius(y, r) < 5e-3
