@@ -108,7 +108,9 @@ def test_quantize_weight_nonfinite_status(fireq):
                                         (5, 14336, True),
                                         # M > 64: the persistent TMA-ring kernel (S = 8, 3, 2 stages;
                                         # rows per CTA > S, so every stage is reused)
-                                        (2000, 4096, True), (700, 16384, False), (67, 12288, True)])
+                                        (2000, 4096, True), (700, 16384, False), (67, 12288, True),
+                                        # several rows per stage slot: the ring wraps (phase flips)
+                                        (6000, 4096, True), (3000, 11008, False)])
 def test_quantize_act(fireq, M, K, with_c):
     xb = synth.activations(M, K, synth.layer_seed(2, M * 7 + K))
     X = synth.bits_to_f64(xb)
