@@ -156,13 +156,16 @@ def test_quantize_act_exhaustive_bf16(fireq):
     assert np.array_equal(xq.cpu().numpy(), rq)
 
 
-def test_quantize_act_strided(fireq):
-    M, K, ld = 8, 256, 384
+@pytest.mark.parametrize("M,K,ld", [(8, 256, 384), (1500, 4096, 4224), (130, 128, 1024)])
+def test_quantize_act_strided(fireq, M, K, ld):
+    """Row stride ld > K (M > 64: the row-ring kernel's bulk copies start at m * ld; K = 128:
+    most of its threads own no vector)."""
     xb = synth.activations(M, ld, 77)
     Xd = to_dev_bf16(xb)[:, :K]
     xq, beta = fireq.quantize_act(Xd)
     rq, rbeta = oq.quantize_act(synth.bits_to_f64(xb)[:, :K])
     assert np.array_equal(xq.cpu().numpy(), rq)
+    assert np.array_equal(bits_of(beta), nm.bf16_to_bits(rbeta))
 
 
 # ----------------------------------------------------------------- GEMM
